@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SABR calibration engine ("Measurement").
+
+Headline workload (BASELINE.json configs[1], "C2"): static SABR with the
+Hagan/Obloj formula (Eq. 7), parallel SA calibration of every maturity of the
+EUR/USD surface (proj/data/eurusd.csv) with 1e5 chains per GPU.  One step =
+calibrate_static_T1 on each of the 4 slices (t0=2, cooling 0.96, L=100,
+t_min=1e-7 -> 412 temperature levels, 4.1e9 cost-evals per slice per 1e5
+chains).  Metric: SA cost-evals/s (whole job).  Secondary line items: the
+Monte Carlo objective (C4: calibrate_case2_T2 on the T=1 equity slice, 1e5
+paths x 250 steps per cost eval) as path-steps/s, and Case I (C3).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank drives one GPU; chains are split over ranks (weak
+scaling: 1e5 chains per GPU) and the per-level record exchange is NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2_CHAINS_PER_GPU = 100_000
+C2_WORKERS, C2_GROUPS = 12_500, 8
+LEVELS_C1 = 412  # (2 * 0.96^k >= 1e-7)
+
+
+def c2_schedule(n_gpus, seed=1, max_evals=None):
+    import paper_2407_20713_b200 as pkg
+
+    n = C2_CHAINS_PER_GPU * n_gpus
+    return pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=C2_WORKERS * n_gpus,
+                                 groups=C2_GROUPS, t_min=1e-7,
+                                 max_evals=max_evals or (n * 100 * LEVELS_C1 + 1), seed=seed)
+
+
+def c4_setup(levels=2):
+    """C4: calibrate_case2_T2 on the T=1 equity slice, dynamics pinned static."""
+    import paper_2407_20713_b200 as pkg
+
+    eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
+    surf = pkg.VolSurface(eq.spot, [eq.slices[2]])
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0}
+    t_min = 2.0 * 0.96 ** (levels - 1) * 0.999
+    sch = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=t_min, seed=1,
+                                max_evals=10 ** 12)
+    plan = pkg.SimulationPlan(num_paths=100_000, dt=1 / 250, seed=1, rng="xoshiro")
+    return surf, fixed, sch, plan
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def flush_l2(torch, dev):
+    buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    buf.zero_()
+    del buf
+
+
+def surface_bytes(surface):
+    ns, nq = len(surface.slices), surface.total_quotes()
+    return 8 * (4 * nq + 3 * ns) + 4 * (ns + 1)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_20713_b200 as pkg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    eng = pkg.Engine(local, stream=stream.cuda_stream)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(pkg.Engine.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        eng.init_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+    eng.set_profiling(True)
+
+    fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
+    sch = c2_schedule(world)
+
+    def step():
+        """One step: calibrate every EUR/USD slice (C2)."""
+        evals, launches, kms, klaunch, wall, reps = 0, 0, 0.0, 0, 0.0, []
+        for sl in range(len(fx.slices)):
+            t0 = time.perf_counter()
+            rep = eng.calibrate_static_T1(fx, sl, None, sch, None)
+            wall += time.perf_counter() - t0
+            t = eng.last_timing()
+            evals += rep.evals - 1
+            launches += t.total_launches + 3  # + start, vol and surface-upload kernels
+            kms += t.kernel_ms
+            klaunch += t.kernel_launches
+            reps.append(rep)
+        return evals, launches, kms, klaunch, wall, reps
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev_times, walls, evals_tot, launches_tot, kms_tot, klaunch_tot = [], [], 0, 0, 0.0, 0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush_l2(torch, dev)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            evals, launches, kms, kl, wall, reps = step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ev_times.append(e0.elapsed_time(e1) / 1e3)
+            walls.append(wall)
+            evals_tot += evals
+            launches_tot += launches
+            kms_tot += kms
+            klaunch_tot += kl
+    t_dev = sum(ev_times)
+    t_wall = sum(walls)
+    if world > 1:
+        tt = torch.tensor([t_dev, t_wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev, t_wall = tt.tolist()
+    # evals reported by calibrate_* are global (all ranks' chains)
+    value = evals_tot / t_dev
+    e2e = evals_tot / t_wall
+
+    # ---- roofline of the dominant kernel (the SA level kernel) ----
+    peak = float(np.median([fp64_peak(eng) for _ in range(3)]))
+    per_eval = fp64_flops_per_eval()
+    avg_launch_s = (kms_tot / klaunch_tot) / 1e3
+    evals_per_launch = evals_tot / klaunch_tot / world  # this rank's chains
+    achieved = evals_per_launch * per_eval["flops"] / avg_launch_s / 1e12
+    traffic = per_eval.get("dram_bytes_per_launch")
+
+    sec = {}
+    if rank == 0 and world == 1 and not args.no_secondary:
+        sec = secondary(eng, torch, dev, stream)
+
+    line = {
+        "metric": "SA cost-evals/s, static Hagan/Obloj (Eq. 7) calibration, EUR/USD surface, 1e5 chains/GPU",
+        "value": value,
+        "unit": "cost-evals/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_dev / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "reference fixture proj/data/eurusd.csv (4 maturities x 19 strikes), copied to tests/data",
+        "config": {"workload": "C2: calibrate_static_T1 on each EUR/USD slice, 1e5 SA chains per GPU "
+                               f"(workers {C2_WORKERS}x{world}, groups {C2_GROUPS}), t0=2 cooling=0.96 "
+                               "L=100 t_min=1e-7 (412 levels)",
+                   "chains": C2_CHAINS_PER_GPU * world, "levels": LEVELS_C1,
+                   "cost_evals_per_step": evals_tot / args.steps,
+                   "calibration_wall_s": t_wall / (args.steps * len(fx.slices)),
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather per level"},
+        "e2e": {"value": e2e, "unit": "cost-evals/s",
+                "h2d_bytes_per_step": len(fx.slices) * (surface_bytes(pkg.VolSurface(fx.spot, [fx.slices[0]])) + 4 * 8 + 400),
+                "d2h_bytes_per_step": len(fx.slices) * (400 + 8 * LEVELS_C1 + 8 * 19 + 8 * 5)},
+        "gpu_launches": int(launches_tot),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "sa_level_kernel<OBJ_STATIC,4>",
+                     "avg_launch_ms": avg_launch_s * 1e3, "launches": klaunch_tot,
+                     "flops_per_eval": per_eval["flops"], "flops_source": per_eval["source"],
+                     "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "
+                                    "MEASURED_PEAKS.json has no FP64 figure"},
+        "clocks": clocks.summary(),
+    }
+    if sec:
+        line["secondary"] = sec
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(fx)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def fp64_peak(eng):
+    import ctypes as C
+
+    v = C.c_double()
+    eng._check(eng.lib.sabr_bench_fp64_peak(eng.handle, C.byref(v)))
+    return v.value
+
+
+def fp64_flops_per_eval():
+    """FP64 FLOPs per cost-eval of the static level kernel (DFMA = 2), measured
+    by ncu (profiles/fp64_per_eval.json); else the SURVEY 8(d) estimate."""
+    p = os.path.join(ROOT, "profiles", "fp64_per_eval.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"flops": d["c2_flops_per_eval"], "source": d["source"],
+                "dram_bytes_per_launch": d.get("c2_dram_bytes_per_launch")}
+    # ~1180 FP64-pipe instructions per eval at m = 19 (upper bound,
+    # counts one FLOP per instruction)
+    return {"flops": 1180.0, "source": "SURVEY.md 8(d) estimate (FP64-pipe instr, m=19)"}
+
+
+def secondary(eng, torch, dev, stream):
+    """C4 (MC objective) and C3 (Case I) line items, measured once after a warm-up."""
+    import paper_2407_20713_b200 as pkg
+
+    out = {}
+    surf, fixed, sch, plan = c4_setup(levels=2)
+    small = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=32, t_min=1.5, seed=1)
+    eng.calibrate_case2_T2(surf, None, small, plan, fixed)  # warm-up (jump tables, buffers)
+    flush_l2(torch, dev)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = eng.calibrate_case2_T2(surf, None, sch, plan, fixed)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = eng.last_timing()
+    secs = e0.elapsed_time(e1) / 1e3
+    steps_per_eval = 250
+    ps = (rep.evals - 1) * plan.num_paths * steps_per_eval
+    out["c4_mc_calibration"] = {
+        "metric": "MC SABR path-steps/s (calibrate_case2_T2 objective, C4)", "unit": "path-steps/s",
+        "value": ps / secs, "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
+        "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,
+        "steps_per_path": steps_per_eval, "rng": plan.rng, "seconds": secs,
+        "mc_kernel_ms": t.kernel_ms, "mc_launches": t.kernel_launches}
+    # C3: Case I joint calibration, EUR/USD, beta = 1 (acceptance.cpp:317-339 schedule, 1e5 chains)
+    fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
+    s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8, t_min=1e-7,
+                               seed=1, max_evals=10 ** 12)
+    eng.calibrate_dynamic_case1_T1(fx, None, pkg.AnnealingSchedule(t0=2, cooling=0.5, workers=64, t_min=1,
+                                                                   seed=1), {"beta": 1.0})
+    e0.record(stream)
+    rep = eng.calibrate_dynamic_case1_T1(fx, None, s3, {"beta": 1.0})
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    secs = e0.elapsed_time(e1) / 1e3
+    out["c3_case1_calibration"] = {"metric": "SA cost-evals/s, Case I (Eq. 8) joint calibration, EUR/USD, 1e5 chains",
+                                   "unit": "cost-evals/s", "value": (rep.evals - 1) / secs, "seconds": secs,
+                                   "mean_rel_error": rep.mean_rel_error}
+    return out
+
+
+def cpu_baseline(fx):
+    """The compiled reference (oracle/_ref) on the host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import Ref, have_ref
+
+    if not have_ref():
+        return {"value": None, "unit": "cost-evals/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    ref = Ref()
+    threads = ref.max_threads()
+    sch = c2_schedule(1, max_evals=2 * 10 ** 7 + 1)
+    sch.omp_threads = threads
+    t0 = time.perf_counter()
+    rep = ref.calibrate_static_T1(fx, 0, None, sch, None)
+    secs = time.perf_counter() - t0
+    return {"value": (rep.evals - 1) / secs, "unit": "cost-evals/s", "cores": threads, "kind": "reference",
+            "sample": f"calibrate_static_T1(eurusd slice 0), C2 schedule capped at max_evals=2e7 "
+                      f"(first 2 levels, {rep.evals - 1} evals, {secs:.1f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the compiled reference CPU implementation, all host threads."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import Ref, have_ref
+
+    import paper_2407_20713_b200.api as api
+
+    if not have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsabr_ref.so not built"}))
+        return
+    ref = Ref()
+    threads = ref.max_threads()
+    from oracles import ref_parse_surface
+
+    fx = ref_parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
+    sch = c2_schedule(world, max_evals=10 ** 7 + 1)
+    sch.omp_threads = threads
+
+    def step(sl):
+        t0 = time.perf_counter()
+        rep = ref.calibrate_static_T1(fx, sl, None, sch, None)
+        return rep.evals - 1, time.perf_counter() - t0
+
+    for i in range(args.warmup):
+        step(i % 4)
+    ev, secs = 0, 0.0
+    for i in range(args.steps):
+        e, s = step(i % 4)
+        ev += e
+        secs += s
+    value = ev / secs
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "SA cost-evals/s, static Hagan/Obloj (Eq. 7) calibration, EUR/USD surface, 1e5 chains/GPU",
+        "value": value, "unit": "cost-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "reference fixture proj/data/eurusd.csv",
+        "config": {"workload": "C2 (bounded CPU sample: each step = calibrate_static_T1 on one EUR/USD slice "
+                               f"with the C2 schedule capped at max_evals=1e7, {threads} OpenMP threads)"},
+        "cpu_baseline": {"value": value, "unit": "cost-evals/s", "cores": threads, "kind": "reference",
+                         "sample": "1e7 cost-evals per step (first level of the C2 schedule)"},
+        "e2e": {"value": value, "unit": "cost-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

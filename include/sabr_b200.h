@@ -353,6 +353,11 @@ SABR_API sabr_status sabr_surface_csv_read(const char* path, double* spot, doubl
                                            double* rate, double* dividend,
                                            int64_t* quote_offset, double* strike, double* vol);
 
+/* Diagnostics: measured FP64 FMA-pipe peak of the context's GPU in TFLOP/s
+ * (8 independent DFMA chains per thread, 8 CTAs of 256 threads per SM) - the
+ * roofline denominator of the FP64-bound kernels. */
+SABR_API sabr_status sabr_bench_fp64_peak(sabr_ctx* ctx, double* tflops);
+
 /* Black-Scholes call (black_scholes.hpp:7-9), used for the T_II market side. */
 SABR_API sabr_status sabr_black_scholes_call(double spot, double strike, double rate,
                                              double dividend, double maturity, double vol,

@@ -94,6 +94,20 @@ void orc_philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, double
 
 /* ----------------------------------------------------------- analytics --- */
 
+/* Last-bit sensitivity probes (test-only): exp and pow inside the analytics
+ * can be moved by +-k ulps to measure how much a 1-ulp libm difference moves
+ * a cost (the reference's own rounding sensitivity, used as the parity bound
+ * where its closed forms cancel). 0 = the plain libm result. */
+static int g_exp_ulps = 0, g_pow_ulps = 0;
+
+static double nudge(double v, int k) {
+    for (; k > 0; --k) v = nextafter(v, INFINITY);
+    for (; k < 0; ++k) v = nextafter(v, -INFINITY);
+    return v;
+}
+static double pexp(double x) { return nudge(exp(x), g_exp_ulps); }
+static double ppow(double x, double y) { return nudge(pow(x, y), g_pow_ulps); }
+
 /* std::min / std::max / std::clamp exactly as libstdc++ defines them. */
 static inline double smin(double a, double b) { return (b < a) ? b : a; }
 static inline double smax(double a, double b) { return (a < b) ? b : a; }
@@ -118,7 +132,7 @@ double orc_static_implied_vol(const double p[4], double strike, double forward, 
     if (!static_valid(p) || !(strike > 0) || !(forward > 0) || !(T > 0)) return NAN;
     const double alpha = p[0], beta = p[1], nu = p[2], rho = p[3];
     const double one_m_beta = 1.0 - beta;
-    const double omega = pow(forward, one_m_beta) / alpha;
+    const double omega = ppow(forward, one_m_beta) / alpha;
     const double rnw = rho * nu * omega;
     const double nw = nu * omega;
     const double a1 = -0.5 * (one_m_beta - rnw);
@@ -162,20 +176,20 @@ static double horner(const double c[14], double x) {
 /* f_nu1 .. f_eta2, analytics.cpp:47-67 */
 static double f_nu1(double x) {
     if (x < KX_SWITCH) return horner(kSeriesNu1, x);
-    return 6.0 / (x * x * x) * (x * x / 2 - x + 1 - exp(-x));
+    return 6.0 / (x * x * x) * (x * x / 2 - x + 1 - pexp(-x));
 }
 static double f_nu2(double x) {
     if (x < KX_SWITCH) return horner(kSeriesNu2, x);
-    const double e = exp(-x);
+    const double e = pexp(-x);
     return 6.0 / (x * x * x) * (2 * (e - 1) + x * (e + 1));
 }
 static double f_eta1(double x) {
     if (x < KX_SWITCH) return horner(kSeriesEta1, x);
-    return 2.0 / (x * x) * (exp(-x) - (1 - x));
+    return 2.0 / (x * x) * (pexp(-x) - (1 - x));
 }
 static double f_eta2(double x) {
     if (x < KX_SWITCH) return horner(kSeriesEta2, x);
-    const double e = exp(-x);
+    const double e = pexp(-x);
     return 3.0 / (x * x * x * x) * (e * e - 8 * e + 7 + 2 * x * (x - 3));
 }
 
@@ -201,7 +215,7 @@ double orc_dynamic_implied_vol(const double c[4], double alpha, double beta, dou
     if (!(alpha > 0) || !(strike > 0) || !(forward > 0) || !(T > 0)) return NAN;
     const double nu1_sq = c[0], nu2_sq = c[1], eta1 = c[2], eta2_sq = c[3];
     const double one_m_beta = 1.0 - beta;
-    const double omega = pow(forward, one_m_beta) / alpha;
+    const double omega = ppow(forward, one_m_beta) / alpha;
     const double e1w = eta1 * omega;
     const double a1 = 0.5 * (beta - 1.0) + 0.5 * e1w;
     const double a2 = one_m_beta * one_m_beta / 12.0 + (one_m_beta - e1w) / 4.0 +
@@ -282,6 +296,22 @@ double orc_cost_case1(const sabr_surface* s, const double p[6]) {
         sum += part;
     }
     return sum;
+}
+
+/* max |cost(libm +-1 ulp) - cost| over the four (exp, pow) nudges. */
+double orc_cost_sensitivity(int model, const sabr_surface* s, int64_t slice, const double* p) {
+    const double base = model == SABR_MODEL_STATIC ? orc_cost_static(s, slice, p) : orc_cost_case1(s, p);
+    double worst = 0.0;
+    for (int e = -1; e <= 1; e += 2)
+        for (int w = -1; w <= 1; w += 2) {
+            g_exp_ulps = e;
+            g_pow_ulps = w;
+            const double c = model == SABR_MODEL_STATIC ? orc_cost_static(s, slice, p) : orc_cost_case1(s, p);
+            const double d = fabs(c - base);
+            if (d > worst) worst = d;
+        }
+    g_exp_ulps = g_pow_ulps = 0;
+    return worst;
 }
 
 /* ------------------------------------------------------------ annealer --- */

@@ -47,6 +47,8 @@ int orc_case2_feasible(const double p[11]);
 /* Cost functions (proj/src/calibration.cpp:253-275, :300-306, :339-349) */
 double orc_cost_static(const sabr_surface* s, int64_t slice, const double p[4]);
 double orc_cost_case1(const sabr_surface* s, const double p[6]);
+/* |cost change| when exp/pow in the analytics move by one ulp (test bound). */
+double orc_cost_sensitivity(int model, const sabr_surface* s, int64_t slice, const double* p);
 
 /* Annealer (proj/src/annealer.cpp:60-167) on a C objective. */
 typedef double (*orc_objective)(const double* x, void* user);

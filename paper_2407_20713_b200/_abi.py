@@ -186,7 +186,7 @@ EXPORTS = [
     "sabr_case2_feasible_batch", "sabr_mc_simulate_terminals",
     "sabr_mc_price_european_batch", "sabr_mc_price_cliquet", "sabr_minimize_builtin",
     "sabr_merge_level_records", "sabr_surface_csv_dims", "sabr_surface_csv_read",
-    "sabr_black_scholes_call",
+    "sabr_black_scholes_call", "sabr_bench_fp64_peak",
 ]
 
 _lib = None

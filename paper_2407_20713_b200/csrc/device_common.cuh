@@ -1,0 +1,365 @@
+// device_common.cuh — sm_100a device primitives of the SABR engine.
+//
+// RNG (reference streams + Philox), the asymptotic implied-vol building
+// blocks and the level-merge rule shared by the host and the device.  Every
+// function cites the reference line it reproduces (paths relative to
+// /root/reference).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sabr_b200.h"
+
+#define SABR_HD __host__ __device__ __forceinline__
+#define SABR_D __device__ __forceinline__
+
+namespace sabr_dev {
+
+// ------------------------------------------------------------------ RNG ---
+
+// splitmix64, proj/include/sabr/rng.hpp:7-12
+SABR_HD uint64_t splitmix64(uint64_t& state) {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+SABR_HD uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+// Xoshiro256pp, rng.hpp:16-43; state kept in four registers.
+struct Xoshiro {
+    uint64_t s0, s1, s2, s3;
+
+    // Xoshiro256pp(seed, stream), rng.hpp:19-23
+    SABR_HD void init(uint64_t seed, uint64_t stream) {
+        uint64_t sm = seed ^ (stream * 0xD2B74407B1CE6E93ull + 0x9E3779B97F4A7C15ull);
+        s0 = splitmix64(sm);
+        s1 = splitmix64(sm);
+        s2 = splitmix64(sm);
+        s3 = splitmix64(sm);
+    }
+    // the F2-linear state transition of next() without the output scrambler
+    SABR_HD void advance() {
+        const uint64_t t = s1 << 17;
+        s2 ^= s0;
+        s3 ^= s1;
+        s1 ^= s2;
+        s0 ^= s3;
+        s2 ^= t;
+        s3 = rotl64(s3, 45);
+    }
+    // next(), rng.hpp:29-39
+    SABR_HD uint64_t next() {
+        const uint64_t result = rotl64(s0 + s3, 23) + s0;
+        advance();
+        return result;
+    }
+    // uniform(), rng.hpp:42: (next() >> 11) * 2^-53 (exact conversion)
+    SABR_HD double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+
+    // state <- M^k state, where x^k mod P(x) = sum_i poly_i x^i (256 bits,
+    // host-computed; see xoshiro_jump.cpp).  Branch-free masked accumulate.
+    SABR_HD void jump(const uint64_t poly[4]) {
+        uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 1
+        for (int w = 0; w < 4; ++w) {
+            const uint64_t word = poly[w];
+#pragma unroll 8
+            for (int b = 0; b < 64; ++b) {
+                const uint64_t m = 0ull - ((word >> b) & 1ull);
+                a0 ^= s0 & m;
+                a1 ^= s1 & m;
+                a2 ^= s2 & m;
+                a3 ^= s3 & m;
+                advance();
+            }
+        }
+        s0 = a0;
+        s1 = a1;
+        s2 = a2;
+        s3 = a3;
+    }
+};
+
+// Philox4x32-10, counter (path lo, path hi, step, 0), key = seed.  The CPU
+// twin is oracle/sabr_oracle.c:orc_philox4x32.
+SABR_D void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t key,
+                          uint32_t out[4]) {
+    uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, double& ua,
+                                double& ub) {
+    uint32_t x[4];
+    philox4x32_10(static_cast<uint32_t>(path), static_cast<uint32_t>(path >> 32), step, 0u, seed, x);
+    const uint64_t a = (static_cast<uint64_t>(x[0]) << 32) | x[1];
+    const uint64_t b = (static_cast<uint64_t>(x[2]) << 32) | x[3];
+    ua = static_cast<double>(a >> 11) * 0x1.0p-53;
+    ub = static_cast<double>(b >> 11) * 0x1.0p-53;
+}
+
+// Box-Muller on two uniforms, proj/src/mc.cpp:30-36.  theta = 2*pi*u2 is
+// evaluated as sincospi(2*u2) (2*u2 is exact), i.e. without the rounding of
+// the 2*pi product; differences are below 1e-15 absolute in z.
+SABR_D void box_muller(double ua, double ub, double& z1, double& z2) {
+    const double u1 = 1.0 - ua;
+    const double r = sqrt(-2.0 * log(u1));
+    double s, c;
+    sincospi(2.0 * ub, &s, &c);
+    z1 = r * c;
+    z2 = r * s;
+}
+
+// ------------------------------------------------------------ analytics ---
+
+// Round-to-nearest primitives that the compiler may not contract into FMAs:
+// the Case I closed forms cancel catastrophically just above the series
+// switch (x = decay*T in [0.25, ~1]: up to 6e3x for f_eta2), so they are
+// evaluated with the reference's exact operation order and roundings.
+#ifdef __CUDA_ARCH__
+#define SABR_ADD(a, b) __dadd_rn((a), (b))
+#define SABR_SUB(a, b) __dsub_rn((a), (b))
+#define SABR_MUL(a, b) __dmul_rn((a), (b))
+#define SABR_DIV(a, b) __ddiv_rn((a), (b))
+#else
+#define SABR_ADD(a, b) ((a) + (b))
+#define SABR_SUB(a, b) ((a) - (b))
+#define SABR_MUL(a, b) ((a) * (b))
+#define SABR_DIV(a, b) ((a) / (b))
+#endif
+
+// Taylor tables of the scaled Case I functions, analytics.cpp:23-39, as
+// fully unrolled Horner evaluations (analytics.cpp:41-45).
+template <int N>
+SABR_HD double horner(const double (&c)[N], double x) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) acc = SABR_ADD(SABR_MUL(acc, x), c[i]);
+    return acc;
+}
+
+SABR_HD double series_nu1(double x) {
+    constexpr double c[14] = {
+        1.0, -1.0 / 4, 1.0 / 20, -1.0 / 120, 1.0 / 840, -1.0 / 6720, 1.0 / 60480,
+        -1.0 / 604800, 1.0 / 6652800, -1.0 / 79833600, 1.0 / 1037836800,
+        -1.0 / 14529715200.0, 1.0 / 217945728000.0, -1.0 / 3487131648000.0};
+    return horner(c, x);
+}
+SABR_HD double series_nu2(double x) {
+    constexpr double c[14] = {
+        1.0, -1.0 / 2, 3.0 / 20, -1.0 / 30, 1.0 / 168, -1.0 / 1120, 1.0 / 8640,
+        -1.0 / 75600, 1.0 / 739200, -1.0 / 7983360, 1.0 / 94348800,
+        -1.0 / 1210809600, 1.0 / 16765056000.0, -1.0 / 249080832000.0};
+    return horner(c, x);
+}
+SABR_HD double series_eta1(double x) {
+    constexpr double c[14] = {
+        1.0, -1.0 / 3, 1.0 / 12, -1.0 / 60, 1.0 / 360, -1.0 / 2520, 1.0 / 20160,
+        -1.0 / 181440, 1.0 / 1814400, -1.0 / 19958400, 1.0 / 239500800,
+        -1.0 / 3113510400.0, 1.0 / 43589145600.0, -1.0 / 653837184000.0};
+    return horner(c, x);
+}
+SABR_HD double series_eta2(double x) {
+    constexpr double c[14] = {
+        1.0, -3.0 / 5, 7.0 / 30, -1.0 / 14, 31.0 / 1680, -1.0 / 240,
+        127.0 / 151200, -17.0 / 110880, 73.0 / 2851200, -31.0 / 7862400,
+        2047.0 / 3632428800.0, -1.0 / 13305600, 8191.0 / 871782912000.0,
+        -5461.0 / 4940103168000.0};
+    return horner(c, x);
+}
+
+// dyn_coeffs_case1 (analytics.cpp:207-215 with f_nu1..f_eta2 :47-67), same
+// operation order and roundings as the reference; exp(-x) is shared by the
+// two functions of one argument (the reference evaluates it twice, same value).
+SABR_HD void dyn_coeffs_case1(double rho0, double nu0, double a, double b, double T,
+                              double& nu1_sq, double& nu2_sq, double& eta1, double& eta2_sq) {
+    constexpr double kXSwitch = 0.25;  // analytics.cpp:21
+    const double xb = SABR_MUL(SABR_MUL(2.0, b), T);
+    const double xab = SABR_MUL(SABR_ADD(a, b), T);
+    const double nn = SABR_MUL(nu0, nu0);
+    const double nr = SABR_MUL(nu0, rho0);
+    double f1, f2, g1, g2;
+    if (xb < kXSwitch) {
+        f1 = series_nu1(xb);
+        f2 = series_nu2(xb);
+    } else {
+        const double e = exp(-xb);
+        const double x2 = SABR_MUL(xb, xb);
+        const double c6 = SABR_DIV(6.0, SABR_MUL(x2, xb));
+        // 6/(x^3) * (x*x/2 - x + 1 - e)
+        f1 = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_DIV(x2, 2.0), xb), 1.0), e));
+        // 6/(x^3) * (2*(e-1) + x*(e+1))
+        f2 = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(xb, SABR_ADD(e, 1.0))));
+    }
+    if (xab < kXSwitch) {
+        g1 = series_eta1(xab);
+        g2 = series_eta2(xab);
+    } else {
+        const double e = exp(-xab);
+        const double x2 = SABR_MUL(xab, xab);
+        // 2/(x*x) * (e - (1 - x))
+        g1 = SABR_MUL(SABR_DIV(2.0, x2), SABR_SUB(e, SABR_SUB(1.0, xab)));
+        // 3/(x*x*x*x) * (e*e - 8*e + 7 + 2*x*(x - 3))
+        const double x4 = SABR_MUL(SABR_MUL(x2, xab), xab);
+        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
+                                     SABR_MUL(SABR_MUL(2.0, xab), SABR_SUB(xab, 3.0)));
+        g2 = SABR_MUL(SABR_DIV(3.0, x4), poly);
+    }
+    nu1_sq = SABR_MUL(nn, f1);
+    nu2_sq = SABR_MUL(nn, f2);
+    eta1 = SABR_MUL(nr, g1);
+    eta2_sq = SABR_MUL(SABR_MUL(nr, nr), g2);
+}
+
+// The maturity-dependent part of Eq. 7 / Eq. 8 hoisted per (candidate,
+// slice): sigma(K) = (c0 + a1*lm + a2*lm^2) * inv_omega with lm = ln(K/f).
+struct SmileTerms {
+    double c0, a1, a2, inv_omega;
+};
+
+// static_implied_vol, analytics.cpp:183-205 (everything that does not depend
+// on the strike).  pw = pow(f, 1-beta).
+SABR_HD SmileTerms static_terms(double alpha, double beta, double nu, double rho, double pw,
+                                double T) {
+    const double one_m_beta = 1.0 - beta;
+    const double omega = pw / alpha;
+    const double inv_omega = 1.0 / omega;
+    const double rnw = rho * nu * omega;
+    const double nw = nu * omega;
+    const double rr = 2.0 - 3.0 * rho * rho;
+    SmileTerms t;
+    t.a1 = -0.5 * (one_m_beta - rnw);
+    t.a2 = (one_m_beta * one_m_beta + 3.0 * (one_m_beta - rnw) + rr * nw * nw) * (1.0 / 12.0);
+    const double b = one_m_beta * one_m_beta * (inv_omega * inv_omega) * (1.0 / 24.0) +
+                     beta * rho * nu * inv_omega * 0.25 + rr * nu * nu * (1.0 / 24.0);
+    t.c0 = 1.0 + b * T;
+    t.inv_omega = inv_omega;
+    return t;
+}
+
+// dynamic_implied_vol, analytics.cpp:291-312 (strike-independent part).
+SABR_HD SmileTerms dynamic_terms(double nu1_sq, double nu2_sq, double eta1, double eta2_sq,
+                                 double alpha, double beta, double pw, double T) {
+    const double one_m_beta = 1.0 - beta;
+    const double omega = pw / alpha;
+    const double inv_omega = 1.0 / omega;
+    const double e1w = eta1 * omega;
+    SmileTerms t;
+    t.a1 = 0.5 * (beta - 1.0) + 0.5 * e1w;
+    t.a2 = one_m_beta * one_m_beta * (1.0 / 12.0) + (one_m_beta - e1w) * 0.25 +
+           (4.0 * nu1_sq + 3.0 * (eta2_sq - 3.0 * eta1 * eta1)) * omega * omega * (1.0 / 24.0);
+    const double b = one_m_beta * one_m_beta * (inv_omega * inv_omega) * (1.0 / 24.0) +
+                     beta * eta1 * inv_omega * 0.25 + (2.0 * nu2_sq - 3.0 * eta2_sq) * (1.0 / 24.0);
+    t.c0 = 1.0 + b * T;
+    t.inv_omega = inv_omega;
+    return t;
+}
+
+SABR_HD double smile_vol(const SmileTerms& t, double lm, double lm2) {
+    return (t.c0 + t.a1 * lm + t.a2 * lm2) * t.inv_omega;
+}
+
+// CaseIIParams::rho_at / nu_at, analytics.cpp:138-143.
+// p = {alpha,beta,rho0,q_rho,d_rho,nu0,q_nu,d_nu,a,b,horizon}
+SABR_HD double case2_rho_at(const double* p, double t) {
+    return (p[2] + p[3] * t) * exp(-p[8] * t) + p[4];
+}
+SABR_HD double case2_nu_at(const double* p, double t) {
+    return (p[5] + p[6] * t) * exp(-p[9] * t) + p[7];
+}
+
+// CaseIIParams::validate as a predicate (case2_feasible), analytics.cpp:145-175,
+// calibration.cpp:161-168: the identical 256-node grid on (0, horizon] plus
+// the two stationary points, with the same 1e-9 rho tolerance.
+SABR_HD bool case2_feasible(const double* p) {
+    const double alpha = p[0], beta = p[1], a = p[8], b = p[9], horizon = p[10];
+    if (!(alpha > 0) || !(beta >= 0 && beta <= 1) || !(a >= 0 && b >= 0) || !(horizon > 0))
+        return false;
+    constexpr double kLo = -1 - 1e-9, kHi = 1 + 1e-9;
+    bool ok = true;
+    for (int i = 1; i <= 256; ++i) {
+        const double t = horizon * i / 256;
+        const double r = case2_rho_at(p, t);
+        ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+    }
+    if (a > 0 && p[3] != 0) {
+        const double t = 1.0 / a - p[2] / p[3];
+        if (t > 0 && t <= horizon) {
+            const double r = case2_rho_at(p, t);
+            ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+        }
+    }
+    if (b > 0 && p[6] != 0) {
+        const double t = 1.0 / b - p[5] / p[6];
+        if (t > 0 && t <= horizon) {
+            const double r = case2_rho_at(p, t);
+            ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+        }
+    }
+    return ok;
+}
+
+// ------------------------------------------------------ level merge rule ---
+
+// (value, global chain index) lexicographic order: strict '<' on the value
+// with the lowest chain winning ties reproduces the sequential scans of
+// proj/src/annealer.cpp:141-159 for any split of the chains.
+SABR_HD bool lex_less(double v, int64_t i, double w, int64_t j) {
+    return v < w || (v == w && i < j);
+}
+
+// One level's cross-rank merge (annealer.cpp:141-160) applied to the state;
+// identical on host (CPU tests, sabr_merge_level_records) and device.
+SABR_HD void merge_level(sabr_sa_state* st, const sabr_level_record* rec, int64_t nranks,
+                         int64_t n_chains, int64_t max_evals, int64_t levels_total, int dim,
+                         double* trace_f) {
+    int64_t e = -1, b = -1, evals = 0;
+    for (int64_t r = 0; r < nranks; ++r) {
+        if (rec[r].end_chain >= 0 &&
+            (e < 0 || lex_less(rec[r].end_value, rec[r].end_chain, rec[e].end_value, rec[e].end_chain)))
+            e = r;
+        if (rec[r].best_chain >= 0 &&
+            (b < 0 ||
+             lex_less(rec[r].best_value, rec[r].best_chain, rec[b].best_value, rec[b].best_chain)))
+            b = r;
+        evals += rec[r].evals;
+    }
+    if (e >= 0 && rec[e].end_value < st->incumbent_value) {
+        st->incumbent_value = rec[e].end_value;
+        for (int i = 0; i < dim; ++i) st->incumbent[i] = rec[e].end_point[i];
+    }
+    if (b >= 0 && rec[b].best_value < st->best_value) {
+        st->best_value = rec[b].best_value;
+        for (int i = 0; i < dim; ++i) st->best[i] = rec[b].best_point[i];
+    }
+    st->evals += evals;
+    if (trace_f) *trace_f = st->incumbent_value;
+    st->levels_run += 1;
+    if (st->levels_run >= levels_total || st->evals >= max_evals) {
+        st->done = 1;
+    } else {
+        const int64_t remaining = max_evals - st->evals;
+        st->eval_cap = (remaining + n_chains - 1) / n_chains;
+    }
+}
+
+}  // namespace sabr_dev

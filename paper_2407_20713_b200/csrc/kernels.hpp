@@ -1,0 +1,117 @@
+// kernels.hpp — host-visible launchers of the sm_100a kernels (internal).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sabr_b200.h"
+
+namespace sabr_gpu {
+
+// Market grid in device memory (SoA, one contiguous allocation).  For the
+// static T_I objective the view covers the calibrated slice only.
+struct SurfaceView {
+    int32_t n_slices;
+    int32_t n_quotes;
+    const double* T;       // [n_slices] maturity
+    const double* lnf_hi;  // [n_slices] ln(forward), double-double
+    const double* lnf_lo;  // [n_slices]
+    const int32_t* qoff;   // [n_slices+1]
+    // [n_quotes] x {lm = ln(K/f) (std::log(strike/forward), the reference
+    // expression, evaluated on the host), lm*lm, market value, 1/market}
+    const double* quotes;
+};
+
+enum ObjectiveKind : int32_t {
+    OBJ_STATIC = 0,   // cost_individual o static_implied_vol       calibration.cpp:300-306
+    OBJ_CASE1 = 1,    // sum_i cost_individual o dynamic_implied_vol calibration.cpp:339-349
+    OBJ_BUILTIN = 2,  // test_annealer.cpp closed forms
+};
+
+struct SaLevelArgs {
+    double lo[SABR_MAX_DIM];
+    double hi[SABR_MAX_DIM];
+    double range[SABR_MAX_DIM];  // hi - lo (annealer.cpp:65)
+    uint32_t free_mask;          // bit i: full-vector dim i is searched
+    int32_t dim_full;
+    int32_t chain_length;
+    int32_t builtin;             // sabr_builtin_objective when OBJ_BUILTIN
+    int32_t predicate;           // SABR_PRED_*
+    int32_t nranks;
+    double t0;
+    uint64_t seed;
+    int64_t chain_begin;         // global index of this rank's first chain
+    int64_t n_local;             // chains on this rank
+    int64_t n_chains;            // global chain count
+    int64_t max_evals;
+    int64_t levels_total;
+    sabr_sa_state* state;        // device
+    sabr_level_record* block_recs;  // [grid] scratch
+    sabr_level_record* rank_rec;    // [1] this rank's record (NCCL send buffer)
+    unsigned int* ticket;           // [1] zero-initialised
+    double* trace_f;                // [levels_total] device
+};
+
+// Launch one temperature level (proj/src/annealer.cpp:99-161).  With nranks==1
+// the merge into `state` happens inside the kernel's last block.
+cudaError_t launch_sa_level(int kind, const SurfaceView& sv, const SaLevelArgs& a, int64_t level,
+                            double temp, cudaStream_t s);
+// Merge `nranks` gathered records into the state (multi-rank path).
+cudaError_t launch_sa_merge(const SaLevelArgs& a, const sabr_level_record* recs, int64_t level,
+                            cudaStream_t s);
+// Evaluate the objective at state->incumbent and seed incumbent/best values.
+cudaError_t launch_sa_start(int kind, const SurfaceView& sv, const SaLevelArgs& a,
+                            cudaStream_t s);
+// cost[i] of full parameter vectors params[i*dim_full ..].
+cudaError_t launch_cost_batch(int kind, const SurfaceView& sv, const double* params,
+                              int32_t dim_full, int64_t n, double* cost, cudaStream_t s);
+// model vols[i*n_quotes + j] for all quotes of the view.
+cudaError_t launch_vol_batch(int kind, const SurfaceView& sv, const double* params,
+                             int32_t dim_full, int64_t n, double* vols, cudaStream_t s);
+cudaError_t launch_case2_feasible(const double* params, int64_t n, uint8_t* out,
+                                  cudaStream_t s);
+
+int sa_block_threads();
+
+// ----------------------------------------------------------- T_II chains ---
+// Chain state of the Monte Carlo objective annealer, kept in HBM between the
+// per-step kernels (propose -> coefficients -> MC -> Metropolis).
+struct T2Chain {
+    double x[SABR_MAX_DIM];   // current point (full parameter vector)
+    double y[SABR_MAX_DIM];   // proposal of this step
+    double bp[SABR_MAX_DIM];  // chain best point
+    double fx, bv;
+    uint64_t rng[4];          // xoshiro256++ state, keyed (seed, level<<20 ^ chain)
+    long long evals;
+    int32_t active;           // proposal of this step is feasible and evaluated
+    int32_t pad;
+};
+
+struct T2StepArgs {
+    double lo[SABR_MAX_DIM], hi[SABR_MAX_DIM], range[SABR_MAX_DIM];
+    uint32_t free_mask;
+    int32_t n_local;
+    double t0, temp, horizon;
+    uint64_t seed;
+    int64_t chain_begin;
+    int64_t level;
+};
+
+cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
+                                 cudaStream_t s);
+// propose + feasibility (analytics.cpp:145-175 on the grid), writes the MC
+// candidate arrays (alpha0, beta, active) for this step.
+cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
+                              double* alpha0, double* beta, uint8_t* active, cudaStream_t s);
+// per (candidate, step) coefficients of build_grid (mc.cpp:69-82) on device
+cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
+                           const double* t_end, const double* dt, const double* sdt,
+                           int64_t total_steps, void* coef, cudaStream_t s);
+// Metropolis (annealer.cpp:123-134) with the MC costs of this step
+cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double* cost,
+                             const int* bad, int* nonfinite, cudaStream_t s);
+// level-end reduction of the chains into the annealer state (as sa_level)
+cudaError_t launch_t2_level_end(const T2Chain* chains, const SaLevelArgs& a, int64_t level,
+                                cudaStream_t s);
+
+}  // namespace sabr_gpu

@@ -1,0 +1,246 @@
+// kernels_mc.cu — fused log-Euler SABR Monte Carlo on sm_100a.
+//
+// One thread simulates `ppt` consecutive paths of one maturity slice for a
+// group of CB candidate parameter sets at once: the two uniforms and the
+// Box-Muller normals of a path-step are drawn once and shared by all CB
+// candidates (the reference's common random numbers: every candidate and
+// every slice restarts the same streams, calibration.cpp:404-409, mc.cpp:127).
+// Per candidate the scheme is the reference log-Euler step (mc.cpp:87-107)
+// carried in log space for the forward (one exp per candidate-step; F_T =
+// F_0 exp(sum)).  Payoffs are reduced in-kernel (warp shuffles -> per-warp
+// shared accumulators -> one partial per 128*ppt-path tile); a second kernel
+// sums the tiles in fixed order.  The reduction tree depends only on
+// (num_paths, ppt), so a candidate's price is a pure function of its
+// parameters and the plan - never of the batch it was launched in.
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "kernels_mc.hpp"
+
+namespace sabr_gpu {
+
+using namespace sabr_dev;
+
+namespace {
+
+constexpr int kWarps = kMcThreads / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    return v;
+}
+
+template <int CB>
+__global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
+    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
+
+    int64_t idx = blockIdx.x;
+    const int tile = static_cast<int>(idx % P.n_tiles);
+    idx /= P.n_tiles;
+    const int s = static_cast<int>(idx % P.n_slices);
+    const int g = static_cast<int>(idx / P.n_slices);
+    const McSlice sl = P.slices[s];
+    const int c0 = g * CB;
+    const int mq = sl.q_end - sl.q_begin;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    bool act[CB];
+    bool logn[CB];
+    double bm1[CB], a0[CB];
+    int n_act = 0;
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+        const int c = c0 + cc;
+        act[cc] = c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
+        n_act += act[cc];
+        const double beta = act[cc] ? P.beta[c] : 1.0;
+        logn[cc] = beta == 1.0;  // mc.cpp:58 fast path
+        bm1[cc] = beta - 1.0;
+        a0[cc] = act[cc] ? (logn[cc] ? P.alpha0[c] : log(P.alpha0[c])) : 0.0;
+    }
+    if (n_act == 0) return;
+
+    const bool reduce = P.partials != nullptr;
+    if (reduce) {
+        for (int i = threadIdx.x; i < kWarps * CB * mq * 2; i += kMcThreads) acc[i] = 0.0;
+        __syncthreads();
+    }
+
+    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
+    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+
+    Xoshiro rng;
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        // block b of the plan, mc.cpp:126-127; jump to this thread's first path
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t k = (p0 % P.block_size) / P.ppt;
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
+
+    const StepCoef* __restrict__ coef = P.coef + sl.step_off;
+    const double* __restrict__ hdt = P.hdt + sl.step_off;
+
+    for (int k = 0; k < P.ppt; ++k) {
+        const uint64_t path = p0 + k;
+        const bool live = path < P.num_paths;
+        double a[CB], x[CB];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            a[cc] = a0[cc];
+            x[cc] = 0.0;
+        }
+        if (live) {
+            for (int i = 0; i < sl.n_steps; ++i) {
+                double ua, ub;
+                if (P.rng == SABR_RNG_XOSHIRO) {
+                    ua = rng.uniform();
+                    ub = rng.uniform();
+                } else {
+                    philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
+                }
+                double z1, z2;
+                box_muller(ua, ub, z1, z2);
+                const double h = __ldg(hdt + i);
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) {
+                    if (!act[cc]) continue;
+                    const StepCoef q = coef[static_cast<int64_t>(c0 + cc) * P.total_steps + i];
+                    double nh;
+                    if (logn[cc]) {  // nu_hat = alpha (mc.cpp:99-100)
+                        nh = a[cc];
+                        a[cc] *= exp(q.c1 * z1 - q.c2);
+                    } else {          // nu_hat = alpha F^(beta-1), alpha carried as ln alpha
+                        nh = exp(a[cc] + bm1[cc] * (sl.lnf0 + x[cc]));
+                        a[cc] += q.c1 * z1 - q.c2;
+                    }
+                    x[cc] += nh * (q.rs * z1 + q.ss * z2) - nh * nh * h;
+                }
+            }
+        }
+        double F[CB];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            F[cc] = sl.forward0 * exp(x[cc]);
+            if (live && act[cc] && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);  // mc.cpp:133-138
+        }
+        if (P.terminals != nullptr && live) P.terminals[path] = F[0];
+        if (!reduce) continue;
+        // discounted call payoffs, mc.cpp:265-269, reduced over the warp
+        for (int j = 0; j < mq; ++j) {
+            const double K = __ldg(P.strikes + sl.q_begin + j);
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) {
+                if (!act[cc]) continue;
+                const double d = F[cc] - K;
+                const double v = live ? sl.discount * ((d < 0.0) ? 0.0 : d) : 0.0;
+                const double s1 = warp_sum(v);
+                const double s2 = warp_sum(v * v);
+                if (lane == 0) {
+                    double* slot = acc + ((warp * CB + cc) * mq + j) * 2;
+                    slot[0] += s1;
+                    slot[1] += s2;
+                }
+            }
+        }
+    }
+    if (!reduce) return;
+    __syncthreads();
+    // warps in fixed order -> one partial per (candidate, quote, tile)
+    for (int t = threadIdx.x; t < CB * mq; t += kMcThreads) {
+        const int cc = t / mq, j = t % mq;
+        if (c0 + cc >= P.n_cand) continue;
+        double s1 = 0.0, s2 = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            s1 += acc[((w * CB + cc) * mq + j) * 2];
+            s2 += acc[((w * CB + cc) * mq + j) * 2 + 1];
+        }
+        double* out = P.partials +
+                      ((static_cast<int64_t>(c0 + cc) * P.n_quotes + sl.q_begin + j) * P.n_tiles + tile) * 2;
+        out[0] = s1;
+        out[1] = s2;
+    }
+}
+
+// reduce_payoffs (mc.cpp:146-157) over the tiles, in tile order.
+__global__ void mc_reduce_kernel(const McParams P, double* __restrict__ value,
+                                 double* __restrict__ std_error) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(P.n_cand) * P.n_quotes) return;
+    const int c = static_cast<int>(t / P.n_quotes);
+    if (P.active != nullptr && P.active[c] == 0) return;
+    const double* p = P.partials + t * P.n_tiles * 2;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < P.n_tiles; ++k) {
+        s1 += p[2 * k];
+        s2 += p[2 * k + 1];
+    }
+    const double n = static_cast<double>(P.num_paths);
+    const double mean = s1 / n;
+    const double q = (s2 - n * mean * mean) / (n - 1.0);
+    const double var = (0.0 < q) ? q : 0.0;
+    value[t] = mean;
+    if (std_error) std_error[t] = sqrt(var / n);
+}
+
+// case2_mc_cost, calibration.cpp:410-413: sum over slices and quotes in order.
+__global__ void mc_cost_kernel(const McParams P, const double* __restrict__ value,
+                               const double* __restrict__ market, double* __restrict__ cost) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P.n_cand) return;
+    if (P.active != nullptr && P.active[c] == 0) return;
+    double sum = 0.0;
+    for (int q = 0; q < P.n_quotes; ++q) {
+        const double rel = (market[q] - value[static_cast<int64_t>(c) * P.n_quotes + q]) / market[q];
+        sum += rel * rel;
+    }
+    cost[c] = sum;
+}
+
+template <int CB>
+cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
+    const int mq = p.max_q;
+    const size_t smem = p.partials ? static_cast<size_t>(kWarps) * CB * mq * 2 * sizeof(double) : 0;
+    auto k = mc_tile_kernel<CB>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    const int n_groups = (p.n_cand + CB - 1) / CB;
+    const int64_t blocks = static_cast<int64_t>(p.n_tiles) * p.n_slices * n_groups;
+    if (blocks <= 0) return cudaSuccess;
+    k<<<static_cast<unsigned>(blocks), kMcThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s) {
+    switch (cand_block) {
+        case 1: return tiles_t<1>(p, s);
+        case 2: return tiles_t<2>(p, s);
+        case 4: return tiles_t<4>(p, s);
+        case 8: return tiles_t<8>(p, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mc_reduce(const McParams& p, double* value, double* std_error,
+                             const double* market, double* cost, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(p.n_cand) * p.n_quotes;
+    if (n > 0) {
+        mc_reduce_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(p, value, std_error);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (cost != nullptr && p.n_cand > 0) {
+        mc_cost_kernel<<<(p.n_cand + 127) / 128, 128, 0, s>>>(p, value, market, cost);
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
+}
+
+}  // namespace sabr_gpu

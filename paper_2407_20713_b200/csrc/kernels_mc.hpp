@@ -1,0 +1,66 @@
+// kernels_mc.hpp — host-visible interface of the log-Euler Monte Carlo kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sabr_gpu {
+
+// One maturity slice of a Monte Carlo launch.  Steps of slice s occupy
+// [step_off, step_off + n_steps) of the per-candidate coefficient rows.
+struct McSlice {
+    int32_t n_steps;
+    int32_t step_off;
+    int32_t q_begin;   // strikes [q_begin, q_end) of the launch's strike list
+    int32_t q_end;
+    int64_t jump_off;  // xoshiro mode: first polynomial of this slice's jump table
+    double forward0;   // S*exp((r-y)T), mc.cpp:258
+    double lnf0;       // log(forward0)
+    double discount;   // exp(-rT), mc.cpp:262
+};
+
+// Per-step, per-candidate log-Euler coefficients (mc.cpp:97-102) for the
+// grid of build_grid (mc.cpp:50-84):
+//   c1 = nu(t_end)*sqrt(dt), c2 = nu^2*dt/2, rs = rho*sqrt(dt), ss = srho*sqrt(dt)
+struct __align__(16) StepCoef {
+    double c1, c2, rs, ss;
+};
+
+struct McParams {
+    int32_t n_slices;
+    int32_t n_cand;
+    int32_t n_quotes;       // total strikes over slices
+    int32_t max_q;          // largest strike count of one slice
+    int32_t n_tiles;        // path tiles per (candidate, slice)
+    int32_t ppt;            // paths per thread (consecutive, same RNG block)
+    int32_t rng;            // sabr_rng
+    int64_t total_steps;    // row length of coef / hdt
+    uint64_t num_paths;
+    uint64_t block_size;
+    uint64_t seed;
+    const McSlice* slices;  // [n_slices]
+    const double* alpha0;   // [n_cand]
+    const double* beta;     // [n_cand]
+    const uint8_t* active;  // [n_cand] or null: skip inactive candidates
+    const StepCoef* coef;   // [n_cand][total_steps]
+    const double* hdt;      // [total_steps] dt/2
+    const double* strikes;  // [n_quotes]
+    const uint64_t* jump;   // xoshiro jump polynomials, 4 words each
+    double* partials;       // [n_cand][n_quotes][n_tiles][2] (sum, sum of squares) or null
+    double* terminals;      // [num_paths] (n_cand == 1, n_slices == 1) or null
+    int* bad;               // [n_cand] non-finite flag
+};
+
+constexpr int kMcThreads = 128;
+
+// Simulate + fused payoff reduction per tile (price_european_batch,
+// mc.cpp:249-273) or terminal write (simulate_terminals, mc.cpp:231-240).
+cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s);
+
+// Final fixed-order reduction over tiles -> value/std_error per (cand, quote)
+// (reduce_payoffs, mc.cpp:146-157); optional cost per candidate against
+// market prices (case2_mc_cost, calibration.cpp:399-416).
+cudaError_t launch_mc_reduce(const McParams& p, double* value, double* std_error,
+                             const double* market, double* cost, cudaStream_t s);
+
+}  // namespace sabr_gpu

@@ -1,0 +1,789 @@
+// kernels_sa.cu — synchronous parallel simulated annealing on sm_100a.
+//
+// One thread = one Markov chain (proj/src/annealer.cpp:107-139).  A launch
+// runs one temperature level for all of this rank's chains: chain state
+// (point, value, best point, xoshiro256++ state) lives in registers, the
+// market grid of the objective is staged once per CTA into shared memory, and
+// the level-end reductions of annealer.cpp:141-159 (per-group endpoint
+// minimum, best-ever, eval count) are a deterministic (value, chain-index)
+// arg-min done in-kernel: warp shuffles, then one CTA record, then the last
+// CTA to finish (ticket) reduces the CTA records and - on a single rank -
+// applies the merge to the device-resident annealer state.  The host never
+// synchronises inside the level loop.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+
+namespace sabr_gpu {
+
+using namespace sabr_dev;
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr size_t kSmemStageLimit = 96 * 1024;
+
+// Per-quote market data as one 32-byte record (two LDS.128 per quote).
+struct __align__(16) Quote {
+    double lm, lm2, mkt, inv_mkt;
+};
+
+struct Grid {
+    int ns;
+    const double* T;
+    const double* lnf_hi;
+    const double* lnf_lo;
+    const int32_t* qoff;
+    const Quote* q;
+};
+
+__host__ __device__ inline size_t stage_bytes(int ns, int nq) {
+    return static_cast<size_t>(nq) * sizeof(Quote) + 3 * sizeof(double) * ns +
+           sizeof(int32_t) * (ns + 1) + 16;
+}
+
+// Cooperative copy of the market grid into shared memory ("staged once").
+__device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem, bool use_smem) {
+    Grid g;
+    g.ns = sv.n_slices;
+    if (!use_smem) {  // grid too large for shared memory: read through L1
+        g.T = sv.T;
+        g.lnf_hi = sv.lnf_hi;
+        g.lnf_lo = sv.lnf_lo;
+        g.qoff = sv.qoff;
+        g.q = reinterpret_cast<const Quote*>(sv.quotes);
+        return g;
+    }
+    Quote* q = reinterpret_cast<Quote*>(smem);
+    double* d = reinterpret_cast<double*>(q + sv.n_quotes);
+    int32_t* o = reinterpret_cast<int32_t*>(d + 3 * sv.n_slices);
+    const Quote* src = reinterpret_cast<const Quote*>(sv.quotes);
+    for (int i = threadIdx.x; i < sv.n_quotes; i += blockDim.x) q[i] = src[i];
+    for (int i = threadIdx.x; i < sv.n_slices; i += blockDim.x) {
+        d[i] = sv.T[i];
+        d[sv.n_slices + i] = sv.lnf_hi[i];
+        d[2 * sv.n_slices + i] = sv.lnf_lo[i];
+    }
+    for (int i = threadIdx.x; i <= sv.n_slices; i += blockDim.x) o[i] = sv.qoff[i];
+    __syncthreads();
+    g.q = q;
+    g.T = d;
+    g.lnf_hi = d + sv.n_slices;
+    g.lnf_lo = d + 2 * sv.n_slices;
+    g.qoff = o;
+    return g;
+}
+
+// f^(1-beta) = exp((1-beta) ln f) with ln f carried in double-double, so the
+// result is as accurate as a correctly rounded exp (pow in analytics.cpp:191).
+__device__ __forceinline__ double pow_fwd(double omb, double lnf_hi, double lnf_lo) {
+    const double y = omb * lnf_hi;
+    const double err = fma(omb, lnf_hi, -y) + omb * lnf_lo;
+    const double e = exp(y);
+    return fma(e, err, e);
+}
+
+// Sum of squared relative errors over one slice, calibration.cpp:253-267.
+__device__ __forceinline__ double slice_cost(const SmileTerms& t, const Quote* q, int q0,
+                                             int q1) {
+    double sum = 0.0;
+#pragma unroll 4
+    for (int j = q0; j < q1; ++j) {
+        const Quote qq = q[j];
+        const double sigma = smile_vol(t, qq.lm, qq.lm2);
+        const double rel = (qq.mkt - sigma) * qq.inv_mkt;
+        sum = fma(rel, rel, sum);
+    }
+    return sum;
+}
+
+// Objective of calibrate_static_T1: full vector {alpha, beta, nu, rho} on the
+// (single) slice of the view.  calibration.cpp:300-306, analytics.cpp:183-205.
+__device__ __forceinline__ double static_cost(const double* v, const Grid& g) {
+    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0]);
+    const SmileTerms t = static_terms(v[0], v[1], v[2], v[3], pw, g.T[0]);
+    return slice_cost(t, g.q, g.qoff[0], g.qoff[1]);
+}
+
+// Objective of calibrate_dynamic_case1_T1: {alpha,beta,rho0,nu0,a,b} summed
+// over slices in order.  calibration.cpp:339-349, analytics.cpp:207-215, :291-312.
+__device__ __forceinline__ double case1_cost(const double* v, const Grid& g) {
+    double sum = 0.0;
+    const double omb = 1.0 - v[1];
+    for (int i = 0; i < g.ns; ++i) {
+        const double T = g.T[i];
+        double n1, n2, e1, e2;
+        dyn_coeffs_case1(v[2], v[3], v[4], v[5], T, n1, n2, e1, e2);
+        const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i]);
+        const SmileTerms t = dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, T);
+        sum += slice_cost(t, g.q, g.qoff[i], g.qoff[i + 1]);
+    }
+    return sum;
+}
+
+__device__ __forceinline__ double sq(double x) { return x * x; }
+
+// The closed-form objectives of proj/tests/test_annealer.cpp.
+__device__ double builtin_value(int id, const double* x) {
+    switch (id) {
+        case SABR_OBJ_BOWL3: return sq(x[0] - 1.2) + sq(x[1] + 0.7) + sq(x[2] - 3.4);
+        case SABR_OBJ_ROSENBROCK4: {
+            double v = 0.0;
+            for (int i = 0; i < 3; ++i) v += 100.0 * sq(x[i + 1] - sq(x[i])) + sq(1.0 - x[i]);
+            return v;
+        }
+        case SABR_OBJ_SINQUAD2: return sq(x[0] - 0.3) + 3.0 * sq(x[1] + 2.1) + 0.1 * sin(7.0 * x[0]);
+        case SABR_OBJ_SQUARE1: return sq(x[0]);
+        case SABR_OBJ_COSBOWL2: return sq(x[0]) + sq(x[1]) + cos(3.0 * x[0]);
+        case SABR_OBJ_CORNER2: return sq(x[0] - 2.0) + sq(x[1] - 2.0);
+        case SABR_OBJ_NANRIGHT1: return x[0] > 0.5 ? CUDART_NAN : sq(x[0] + 1.0);
+    }
+    return CUDART_NAN;
+}
+
+template <int KIND>
+__device__ __forceinline__ double objective(const double* v, const Grid& g, int builtin) {
+    if constexpr (KIND == OBJ_STATIC) return static_cost(v, g);
+    else if constexpr (KIND == OBJ_CASE1) return case1_cost(v, g);
+    else return builtin_value(builtin, v);
+}
+
+// SearchSpace::is_feasible minus contains() (a clamped proposal is always in
+// the box): the optional predicate (test_annealer.cpp:108-121).
+__device__ __forceinline__ bool predicate_ok(int pred, const double* y) {
+    if (pred == SABR_PRED_SUM_LE_1) return y[0] + y[1] <= 1.0;
+    return true;
+}
+
+// ------------------------------------------------------- reductions ---
+struct ArgMin {
+    double v;
+    int64_t i;
+    int32_t blk;
+};
+
+__device__ __forceinline__ void argmin_combine(ArgMin& a, const ArgMin& b) {
+    if (lex_less(b.v, b.i, a.v, a.i)) a = b;
+}
+
+__device__ __forceinline__ ArgMin warp_argmin(ArgMin a) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        ArgMin o;
+        o.v = __shfl_down_sync(0xffffffffu, a.v, off);
+        o.i = __shfl_down_sync(0xffffffffu, a.i, off);
+        o.blk = __shfl_down_sync(0xffffffffu, a.blk, off);
+        argmin_combine(a, o);
+    }
+    return a;
+}
+
+__device__ __forceinline__ long long warp_sum(long long x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    return x;
+}
+
+struct RedShared {
+    ArgMin e[kWarps], b[kWarps];
+    long long n[kWarps];
+    ArgMin e_win, b_win;
+    long long n_tot;
+    int is_last;
+};
+
+// Block-wide (endpoint, best) arg-min and eval sum; result valid in `rs`
+// after the call for all threads.
+__device__ void block_reduce(RedShared& rs, ArgMin e, ArgMin b, long long n) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    e = warp_argmin(e);
+    b = warp_argmin(b);
+    n = warp_sum(n);
+    if (lane == 0) {
+        rs.e[warp] = e;
+        rs.b[warp] = b;
+        rs.n[warp] = n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ArgMin ee = rs.e[0], bb = rs.b[0];
+        long long nn = rs.n[0];
+        for (int w = 1; w < kWarps; ++w) {
+            argmin_combine(ee, rs.e[w]);
+            argmin_combine(bb, rs.b[w]);
+            nn += rs.n[w];
+        }
+        rs.e_win = ee;
+        rs.b_win = bb;
+        rs.n_tot = nn;
+    }
+    __syncthreads();
+}
+
+// --------------------------------------------------------- level kernel ---
+template <int KIND, int DIMF>
+__global__ void __launch_bounds__(kThreads)
+    sa_level_kernel(const SurfaceView sv, const SaLevelArgs a, const int64_t level,
+                    const double temp, const int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RedShared rs;
+    __shared__ sabr_level_record rec;
+
+    sabr_sa_state* st = a.state;
+    if (st->done) return;  // early-stopped run (max_evals): uniform exit
+
+    Grid g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_grid(sv, smem, use_smem != 0);
+
+    const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const bool active = local < a.n_local;
+    const int64_t chain = a.chain_begin + local;
+
+    double x[DIMF], y[DIMF], bp[DIMF];
+#pragma unroll
+    for (int i = 0; i < DIMF; ++i) {
+        x[i] = st->incumbent[i];
+        bp[i] = x[i];
+    }
+    double fx = st->incumbent_value;
+    double bv = fx;
+    long long ev = 0;
+    const long long cap = st->eval_cap;
+
+    if (active) {
+        // substream keyed by (seed, level, chain): annealer.cpp:112-115
+        Xoshiro rng;
+        rng.init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain));
+        const double ratio = temp / a.t0;
+        const double scale = (ratio < 1.0) ? ratio : 1.0;  // std::min(1.0, T/t0), annealer.cpp:62
+        for (int step = 0; step < a.chain_length; ++step) {
+            if (ev >= cap) break;  // annealer.cpp:120
+            // propose, annealer.cpp:60-74 (no FMA contraction: bit-identical proposals)
+#pragma unroll
+            for (int i = 0; i < DIMF; ++i) {
+                if ((a.free_mask >> i) & 1u) {
+                    const double u = rng.uniform();
+                    const double stp =
+                        __dmul_rn(__dmul_rn(a.range[i], scale), __dsub_rn(__dmul_rn(2.0, u), 1.0));
+                    double v = __dadd_rn(x[i], stp);
+                    if (v > a.hi[i]) v = __dsub_rn(__dmul_rn(2.0, a.hi[i]), v);
+                    if (v < a.lo[i]) v = __dsub_rn(__dmul_rn(2.0, a.lo[i]), v);
+                    y[i] = (v < a.lo[i]) ? a.lo[i] : (a.hi[i] < v) ? a.hi[i] : v;
+                } else {
+                    y[i] = x[i];
+                }
+            }
+            if (!predicate_ok(a.predicate, y)) continue;  // annealer.cpp:122
+            double fy = objective<KIND>(y, g, a.builtin);
+            if (isnan(fy)) fy = CUDART_INF;  // safe_eval, annealer.cpp:84-87
+            ++ev;
+            // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx)
+            bool accept = fy <= fx;
+            if (!accept) accept = rng.uniform() < exp(-(fy - fx) / temp);
+            if (accept) {
+#pragma unroll
+                for (int i = 0; i < DIMF; ++i) x[i] = y[i];
+                fx = fy;
+                if (fx < bv) {
+                    bv = fx;
+#pragma unroll
+                    for (int i = 0; i < DIMF; ++i) bp[i] = x[i];
+                }
+            }
+        }
+    }
+
+    // ---- level-end reduction (annealer.cpp:141-159) ----
+    ArgMin e{active ? fx : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    ArgMin b{active ? bv : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    block_reduce(rs, e, b, ev);
+    if (active && chain == rs.e_win.i) {
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) rec.end_point[i] = x[i];
+    }
+    if (active && chain == rs.b_win.i) {
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rec.end_value = rs.e_win.v;
+        rec.end_chain = rs.e_win.i == LLONG_MAX ? -1 : rs.e_win.i;
+        rec.best_value = rs.b_win.v;
+        rec.best_chain = rs.b_win.i == LLONG_MAX ? -1 : rs.b_win.i;
+        rec.evals = rs.n_tot;
+        a.block_recs[blockIdx.x] = rec;
+        __threadfence();
+        const unsigned t = atomicAdd(a.ticket, 1u);
+        rs.is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!rs.is_last) return;
+
+    // ---- last CTA: reduce the CTA records of this rank ----
+    __threadfence();
+    ArgMin ee{CUDART_INF, LLONG_MAX, -1}, bb{CUDART_INF, LLONG_MAX, -1};
+    long long nn = 0;
+    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += kThreads) {
+        const sabr_level_record* r = a.block_recs + k;
+        const double rev = __ldcg(&r->end_value);
+        const long long rei = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
+        const double rbv = __ldcg(&r->best_value);
+        const long long rbi = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
+        if (rei >= 0) argmin_combine(ee, ArgMin{rev, rei, k});
+        if (rbi >= 0) argmin_combine(bb, ArgMin{rbv, rbi, k});
+        nn += __ldcg(reinterpret_cast<const long long*>(&r->evals));
+    }
+    block_reduce(rs, ee, bb, nn);
+    if (threadIdx.x == 0) {
+        sabr_level_record out;
+        out.end_value = rs.e_win.v;
+        out.end_chain = rs.e_win.blk >= 0 ? rs.e_win.i : -1;
+        out.best_value = rs.b_win.v;
+        out.best_chain = rs.b_win.blk >= 0 ? rs.b_win.i : -1;
+        out.evals = rs.n_tot;
+        out._pad = 0;
+        for (int i = 0; i < SABR_MAX_DIM; ++i) {
+            out.end_point[i] = rs.e_win.blk >= 0 && i < DIMF
+                                   ? __ldcg(&a.block_recs[rs.e_win.blk].end_point[i]) : 0.0;
+            out.best_point[i] = rs.b_win.blk >= 0 && i < DIMF
+                                    ? __ldcg(&a.block_recs[rs.b_win.blk].best_point[i]) : 0.0;
+        }
+        *a.rank_rec = out;
+        *a.ticket = 0u;
+        if (a.nranks == 1)
+            merge_level(st, &out, 1, a.n_chains, a.max_evals, a.levels_total, DIMF,
+                        a.trace_f + level);
+    }
+}
+
+__global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* recs,
+                                const int64_t level) {
+    if (a.state->done) return;
+    merge_level(a.state, recs, a.nranks, a.n_chains, a.max_evals, a.levels_total, a.dim_full,
+                a.trace_f + level);
+}
+
+template <int KIND, int DIMF>
+__global__ void sa_start_kernel(const SurfaceView sv, const SaLevelArgs a, const int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Grid g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_grid(sv, smem, use_smem != 0);
+    if (threadIdx.x != 0) return;
+    double x[DIMF];
+    for (int i = 0; i < DIMF; ++i) x[i] = a.state->incumbent[i];
+    double v = objective<KIND>(x, g, a.builtin);
+    if (isnan(v)) v = CUDART_INF;
+    a.state->incumbent_value = v;
+    a.state->best_value = v;
+}
+
+template <int KIND, int DIMF>
+__global__ void __launch_bounds__(kThreads)
+    cost_batch_kernel(const SurfaceView sv, const double* __restrict__ params, const int64_t n,
+                      double* __restrict__ cost, const int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Grid g = stage_grid(sv, smem, use_smem != 0);
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    if (i >= n) return;
+    double v[DIMF];
+#pragma unroll
+    for (int k = 0; k < DIMF; ++k) v[k] = params[i * DIMF + k];
+    cost[i] = objective<KIND>(v, g, 0);
+}
+
+// Model vols for every quote of the view (report rows, calibration.cpp:180-194).
+template <int KIND, int DIMF>
+__global__ void vol_batch_kernel(const SurfaceView sv, const double* __restrict__ params,
+                                 const int64_t n, double* __restrict__ vols, const int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Grid g = stage_grid(sv, smem, use_smem != 0);
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v[DIMF];
+#pragma unroll
+    for (int k = 0; k < DIMF; ++k) v[k] = params[i * DIMF + k];
+    const int nq = g.qoff[g.ns];
+    const double omb = 1.0 - v[1];
+    for (int s = 0; s < g.ns; ++s) {
+        const double pw = pow_fwd(omb, g.lnf_hi[s], g.lnf_lo[s]);
+        SmileTerms t;
+        if constexpr (KIND == OBJ_STATIC) {
+            t = static_terms(v[0], v[1], v[2], v[3], pw, g.T[s]);
+        } else {
+            double n1, n2, e1, e2;
+            dyn_coeffs_case1(v[2], v[3], v[4], v[5], g.T[s], n1, n2, e1, e2);
+            t = dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, g.T[s]);
+        }
+        for (int j = g.qoff[s]; j < g.qoff[s + 1]; ++j)
+            vols[i * nq + j] = smile_vol(t, g.q[j].lm, g.q[j].lm2);
+    }
+}
+
+__global__ void case2_feasible_kernel(const double* __restrict__ params, const int64_t n,
+                                      uint8_t* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) p[k] = params[i * 11 + k];
+    out[i] = case2_feasible(p) ? 1 : 0;
+}
+
+
+// ------------------------------------------------------- T_II chain kernels ---
+// propose, annealer.cpp:60-74, over the full vector (fixed dims untouched;
+// uniforms drawn for free dims in order, as the reference's search vector).
+__device__ __forceinline__ void propose_full(const double* x, double* y, const double* lo,
+                                             const double* hi, const double* range,
+                                             uint32_t mask, double scale, Xoshiro& rng) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        if ((mask >> i) & 1u) {
+            const double u = rng.uniform();
+            const double stp = __dmul_rn(__dmul_rn(range[i], scale), __dsub_rn(__dmul_rn(2.0, u), 1.0));
+            double v = __dadd_rn(x[i], stp);
+            if (v > hi[i]) v = __dsub_rn(__dmul_rn(2.0, hi[i]), v);
+            if (v < lo[i]) v = __dsub_rn(__dmul_rn(2.0, lo[i]), v);
+            y[i] = (v < lo[i]) ? lo[i] : (hi[i] < v) ? hi[i] : v;
+        } else {
+            y[i] = x[i];
+        }
+    }
+}
+
+__device__ __forceinline__ void load_rng(Xoshiro& r, const uint64_t* s) {
+    r.s0 = s[0];
+    r.s1 = s[1];
+    r.s2 = s[2];
+    r.s3 = s[3];
+}
+__device__ __forceinline__ void store_rng(const Xoshiro& r, uint64_t* s) {
+    s[0] = r.s0;
+    s[1] = r.s1;
+    s[2] = r.s2;
+    s[3] = r.s3;
+}
+
+__global__ void t2_level_init_kernel(T2Chain* __restrict__ chains, const sabr_sa_state* st,
+                                     const T2StepArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.n_local || st->done) return;
+    T2Chain& ch = chains[c];
+    for (int i = 0; i < SABR_MAX_DIM; ++i) ch.x[i] = ch.bp[i] = ch.y[i] = st->incumbent[i];
+    ch.fx = ch.bv = st->incumbent_value;
+    ch.evals = 0;
+    ch.active = 0;
+    Xoshiro r;
+    r.init(a.seed, (static_cast<uint64_t>(a.level) << 20) ^ static_cast<uint64_t>(a.chain_begin + c));
+    store_rng(r, ch.rng);
+}
+
+__global__ void t2_propose_kernel(T2Chain* __restrict__ chains, const sabr_sa_state* st,
+                                  const T2StepArgs a, double* __restrict__ alpha0,
+                                  double* __restrict__ beta, uint8_t* __restrict__ active) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.n_local) return;
+    T2Chain& ch = chains[c];
+    ch.active = 0;
+    active[c] = 0;
+    if (st->done || ch.evals >= st->eval_cap) return;  // annealer.cpp:120
+    Xoshiro r;
+    load_rng(r, ch.rng);
+    const double ratio = a.temp / a.t0;
+    const double scale = (ratio < 1.0) ? ratio : 1.0;
+    double x[10], y[11];
+    for (int i = 0; i < 10; ++i) x[i] = ch.x[i];
+    propose_full(x, y, a.lo, a.hi, a.range, a.free_mask, scale, r);
+    store_rng(r, ch.rng);
+    y[10] = a.horizon;
+    for (int i = 0; i < 10; ++i) ch.y[i] = y[i];
+    // SearchSpace::is_feasible -> case2_feasible (calibration.cpp:467-469)
+    const bool ok = case2_feasible(y);
+    ch.active = ok ? 1 : 0;
+    active[c] = ok ? 1 : 0;
+    alpha0[c] = y[0];
+    beta[c] = y[1];
+}
+
+__global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t* __restrict__ active,
+                               const int32_t n_local, const double* __restrict__ t_end,
+                               const double* __restrict__ dt, const double* __restrict__ sdt,
+                               const int64_t total_steps, double4* __restrict__ coef) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(n_local) * total_steps) return;
+    const int c = static_cast<int>(t / total_steps);
+    const int64_t i = t % total_steps;
+    if (!active[c]) return;
+    const T2Chain& ch = chains[c];
+    double p[11];
+    for (int k = 0; k < 10; ++k) p[k] = ch.y[k];
+    const double tt = t_end[i];
+    const double nu = case2_nu_at(p, tt);    // nu, rho at the step END, mc.cpp:69-82
+    const double rho = case2_rho_at(p, tt);
+    const double q = 1.0 - rho * rho;
+    const double srho = sqrt((0.0 < q) ? q : 0.0);
+    const double s = sdt[i];
+    coef[t] = make_double4(nu * s, 0.5 * nu * nu * dt[i], rho * s, srho * s);
+}
+
+__global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
+                                 const double* __restrict__ cost, const int* __restrict__ bad,
+                                 int* __restrict__ nonfinite) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.n_local) return;
+    T2Chain& ch = chains[c];
+    if (!ch.active) return;
+    if (bad[c]) atomicOr(nonfinite, 1);
+    double fy = cost[c];
+    if (isnan(fy)) fy = CUDART_INF;
+    ch.evals += 1;
+    bool accept = fy <= ch.fx;
+    if (!accept) {
+        Xoshiro r;
+        load_rng(r, ch.rng);
+        accept = r.uniform() < exp(-(fy - ch.fx) / a.temp);
+        store_rng(r, ch.rng);
+    }
+    if (accept) {
+        for (int i = 0; i < 10; ++i) ch.x[i] = ch.y[i];
+        ch.fx = fy;
+        if (fy < ch.bv) {
+            ch.bv = fy;
+            for (int i = 0; i < 10; ++i) ch.bp[i] = ch.y[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    t2_level_end_kernel(const T2Chain* __restrict__ chains, const SaLevelArgs a, const int64_t level) {
+    __shared__ RedShared rs;
+    __shared__ sabr_level_record rec;
+    sabr_sa_state* st = a.state;
+    if (st->done) return;
+    const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const bool active = local < a.n_local;
+    const int64_t chain = a.chain_begin + local;
+    const T2Chain* ch = active ? chains + local : nullptr;
+    ArgMin e{active ? ch->fx : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    ArgMin b{active ? ch->bv : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    block_reduce(rs, e, b, active ? ch->evals : 0);
+    if (active && chain == rs.e_win.i)
+        for (int i = 0; i < SABR_MAX_DIM; ++i) rec.end_point[i] = ch->x[i];
+    if (active && chain == rs.b_win.i)
+        for (int i = 0; i < SABR_MAX_DIM; ++i) rec.best_point[i] = ch->bp[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rec.end_value = rs.e_win.v;
+        rec.end_chain = rs.e_win.i == LLONG_MAX ? -1 : rs.e_win.i;
+        rec.best_value = rs.b_win.v;
+        rec.best_chain = rs.b_win.i == LLONG_MAX ? -1 : rs.b_win.i;
+        rec.evals = rs.n_tot;
+        a.block_recs[blockIdx.x] = rec;
+        __threadfence();
+        const unsigned t = atomicAdd(a.ticket, 1u);
+        rs.is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!rs.is_last) return;
+    __threadfence();
+    ArgMin ee{CUDART_INF, LLONG_MAX, -1}, bb{CUDART_INF, LLONG_MAX, -1};
+    long long nn = 0;
+    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += kThreads) {
+        const sabr_level_record* r = a.block_recs + k;
+        const double rev = __ldcg(&r->end_value);
+        const long long rei = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
+        const double rbv = __ldcg(&r->best_value);
+        const long long rbi = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
+        if (rei >= 0) argmin_combine(ee, ArgMin{rev, rei, k});
+        if (rbi >= 0) argmin_combine(bb, ArgMin{rbv, rbi, k});
+        nn += __ldcg(reinterpret_cast<const long long*>(&r->evals));
+    }
+    block_reduce(rs, ee, bb, nn);
+    if (threadIdx.x == 0) {
+        sabr_level_record out;
+        out.end_value = rs.e_win.v;
+        out.end_chain = rs.e_win.blk >= 0 ? rs.e_win.i : -1;
+        out.best_value = rs.b_win.v;
+        out.best_chain = rs.b_win.blk >= 0 ? rs.b_win.i : -1;
+        out.evals = rs.n_tot;
+        out._pad = 0;
+        for (int i = 0; i < SABR_MAX_DIM; ++i) {
+            out.end_point[i] = rs.e_win.blk >= 0 ? __ldcg(&a.block_recs[rs.e_win.blk].end_point[i]) : 0.0;
+            out.best_point[i] = rs.b_win.blk >= 0 ? __ldcg(&a.block_recs[rs.b_win.blk].best_point[i]) : 0.0;
+        }
+        *a.rank_rec = out;
+        *a.ticket = 0u;
+        if (a.nranks == 1)
+            merge_level(st, &out, 1, a.n_chains, a.max_evals, a.levels_total, SABR_MAX_DIM,
+                        a.trace_f + level);
+    }
+}
+
+size_t smem_for(const SurfaceView& sv, int* use_smem) {
+    const size_t b = stage_bytes(sv.n_slices, sv.n_quotes);
+    *use_smem = b <= kSmemStageLimit;
+    return *use_smem ? b : 0;
+}
+
+template <class K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(bytes));
+    return cudaSuccess;
+}
+
+template <int KIND, int DIMF>
+cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
+                    cudaStream_t s) {
+    int use = 0;
+    const size_t smem = KIND == OBJ_BUILTIN ? 0 : smem_for(sv, &use);
+    auto k = sa_level_kernel<KIND, DIMF>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>((a.n_local + kThreads - 1) / kThreads);
+    k<<<grid, kThreads, smem, s>>>(sv, a, level, temp, use);
+    return cudaGetLastError();
+}
+
+template <int KIND, int DIMF>
+cudaError_t start_t(const SurfaceView& sv, const SaLevelArgs& a, cudaStream_t s) {
+    int use = 0;
+    const size_t smem = KIND == OBJ_BUILTIN ? 0 : smem_for(sv, &use);
+    auto k = sa_start_kernel<KIND, DIMF>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<1, 32, smem, s>>>(sv, a, use);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int sa_block_threads() { return kThreads; }
+
+#define SABR_DISPATCH(kind, dim, CALL)                                       \
+    do {                                                                     \
+        if (kind == OBJ_STATIC) return CALL(OBJ_STATIC, 4);                  \
+        if (kind == OBJ_CASE1) return CALL(OBJ_CASE1, 6);                    \
+        switch (dim) {                                                       \
+            case 1: return CALL(OBJ_BUILTIN, 1);                             \
+            case 2: return CALL(OBJ_BUILTIN, 2);                             \
+            case 3: return CALL(OBJ_BUILTIN, 3);                             \
+            case 4: return CALL(OBJ_BUILTIN, 4);                             \
+        }                                                                    \
+        return cudaErrorInvalidValue;                                        \
+    } while (0)
+
+cudaError_t launch_sa_level(int kind, const SurfaceView& sv, const SaLevelArgs& a, int64_t level,
+                            double temp, cudaStream_t s) {
+#define CALL(K, D) level_t<K, D>(sv, a, level, temp, s)
+    SABR_DISPATCH(kind, a.dim_full, CALL);
+#undef CALL
+}
+
+cudaError_t launch_sa_start(int kind, const SurfaceView& sv, const SaLevelArgs& a,
+                            cudaStream_t s) {
+#define CALL(K, D) start_t<K, D>(sv, a, s)
+    SABR_DISPATCH(kind, a.dim_full, CALL);
+#undef CALL
+}
+
+cudaError_t launch_sa_merge(const SaLevelArgs& a, const sabr_level_record* recs, int64_t level,
+                            cudaStream_t s) {
+    sa_merge_kernel<<<1, 1, 0, s>>>(a, recs, level);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cost_batch(int kind, const SurfaceView& sv, const double* params,
+                              int32_t dim_full, int64_t n, double* cost, cudaStream_t s) {
+    int use = 0;
+    const size_t smem = smem_for(sv, &use);
+    const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
+    if (kind == OBJ_STATIC && dim_full == 4) {
+        auto k = cost_batch_kernel<OBJ_STATIC, 4>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost, use);
+    } else if (kind == OBJ_CASE1 && dim_full == 6) {
+        auto k = cost_batch_kernel<OBJ_CASE1, 6>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost, use);
+    } else {
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vol_batch(int kind, const SurfaceView& sv, const double* params,
+                             int32_t dim_full, int64_t n, double* vols, cudaStream_t s) {
+    int use = 0;
+    const size_t smem = smem_for(sv, &use);
+    const unsigned grid = static_cast<unsigned>((n + 63) / 64);
+    if (kind == OBJ_STATIC && dim_full == 4) {
+        auto k = vol_batch_kernel<OBJ_STATIC, 4>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, 64, smem, s>>>(sv, params, n, vols, use);
+    } else if (kind == OBJ_CASE1 && dim_full == 6) {
+        auto k = vol_batch_kernel<OBJ_CASE1, 6>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, 64, smem, s>>>(sv, params, n, vols, use);
+    } else {
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_case2_feasible(const double* params, int64_t n, uint8_t* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    case2_feasible_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(params, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
+                                 cudaStream_t s) {
+    if (a.n_local <= 0) return cudaSuccess;
+    t2_level_init_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, st, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
+                              double* alpha0, double* beta, uint8_t* active, cudaStream_t s) {
+    if (a.n_local <= 0) return cudaSuccess;
+    t2_propose_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, st, a, alpha0, beta, active);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
+                           const double* t_end, const double* dt, const double* sdt,
+                           int64_t total_steps, void* coef, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(n_local) * total_steps;
+    if (n <= 0) return cudaSuccess;
+    t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        chains, active, n_local, t_end, dt, sdt, total_steps, static_cast<double4*>(coef));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double* cost,
+                             const int* bad, int* nonfinite, cudaStream_t s) {
+    if (a.n_local <= 0) return cudaSuccess;
+    t2_accept_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, a, cost, bad, nonfinite);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_level_end(const T2Chain* chains, const SaLevelArgs& a, int64_t level,
+                                cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, (a.n_local + kThreads - 1) / kThreads));
+    t2_level_end_kernel<<<grid, kThreads, 0, s>>>(chains, a, level);
+    return cudaGetLastError();
+}
+
+}  // namespace sabr_gpu

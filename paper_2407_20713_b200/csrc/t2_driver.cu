@@ -1,0 +1,215 @@
+// t2_driver.cu — the annealer of calibrate_case2_T2 (proj/src/calibration.cpp:450-481)
+// with its Monte Carlo objective (case2_mc_cost, :399-416) on the device.
+//
+// The reference runs the chains of a level in an OpenMP loop and, inside each
+// chain step, prices every slice with a fresh MC run (nested, serialized).
+// Here the chains step in lockstep: one step of ALL chains is
+//   propose+feasibility (1 thread/chain) -> grid coefficients (1 thread per
+//   candidate-step) -> one batched MC launch over (candidate group x slice x
+//   path tile), sharing the normals of a path-step across the candidates of a
+//   group -> fixed-order tile reduction and cost -> Metropolis (1 thread/chain),
+// and the level ends with the same in-kernel arg-min merge as the T_I driver.
+// Nothing returns to the host inside a level.
+#include <algorithm>
+#include <cmath>
+
+#include "engine.hpp"
+
+namespace sabr_gpu {
+
+AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vector<double>& market,
+                       const ParamSpace& ps, const std::vector<double>& start_full, double horizon,
+                       const sabr_schedule& sch, const sabr_plan& plan) {
+    const std::vector<double> temps = temperatures(sch);
+    const int64_t L = static_cast<int64_t>(temps.size());
+    const int64_t n_chains = static_cast<int64_t>(sch.workers) * sch.groups;
+    const int64_t begin = ctx->rank * n_chains / ctx->nranks;
+    const int64_t end = (ctx->rank + 1) * n_chains / ctx->nranks;
+    const int32_t n_local = static_cast<int32_t>(end - begin);
+    const size_t ns = surface.n();
+    const int nq = static_cast<int>(surface.total_quotes());
+
+    // ---- start value: safe_eval(start), annealer.cpp:90 ----
+    std::vector<double> p0 = start_full;
+    p0.push_back(horizon);
+    double start_value;
+    {
+        std::vector<double> value, se;
+        mc_price_single(ctx, SABR_MODEL_CASE2, p0.data(), surface.spot, surface.T, surface.r, surface.y,
+                        surface.off, surface.K, plan, value, se);
+        double sum = 0.0;
+        for (int q = 0; q < nq; ++q) {
+            const double rel = (market[q] - value[q]) / market[q];
+            sum += rel * rel;
+        }
+        start_value = std::isnan(sum) ? INFINITY : sum;
+    }
+
+    // ---- MC layout shared by every step ----
+    std::vector<HostGrid> grids;
+    for (size_t s = 0; s < ns; ++s) grids.push_back(build_grid(surface.T[s], plan.dt));
+    const int ppt = choose_ppt(plan);
+    McJob job;
+    job.slices.resize(ns);
+    const auto jump = mc_layout(ctx, plan, ppt, grids, job);
+    std::vector<double> t_end, dt, sdt;
+    for (size_t s = 0; s < ns; ++s) {
+        McSlice& sl = job.slices[s];
+        sl.q_begin = static_cast<int32_t>(surface.off[s]);
+        sl.q_end = static_cast<int32_t>(surface.off[s + 1]);
+        job.max_q = std::max(job.max_q, sl.q_end - sl.q_begin);
+        sl.forward0 = surface.spot * std::exp((surface.r[s] - surface.y[s]) * surface.T[s]);  // mc.cpp:258
+        sl.lnf0 = std::log(sl.forward0);
+        sl.discount = std::exp(-surface.r[s] * surface.T[s]);
+        t_end.insert(t_end.end(), grids[s].t_end.begin(), grids[s].t_end.end());
+        dt.insert(dt.end(), grids[s].dt.begin(), grids[s].dt.end());
+        sdt.insert(sdt.end(), grids[s].sdt.begin(), grids[s].sdt.end());
+    }
+    const int64_t S = job.total_steps;
+    const int32_t n_tiles = static_cast<int32_t>(
+        (plan.num_paths + static_cast<uint64_t>(kMcThreads) * ppt - 1) / (static_cast<uint64_t>(kMcThreads) * ppt));
+    // candidates per MC launch: bound the coefficient and partial buffers
+    const int64_t per_cand = S * 32 + static_cast<int64_t>(nq) * n_tiles * 16;
+    const int32_t chunk = static_cast<int32_t>(
+        std::max<int64_t>(1, std::min<int64_t>(std::max(n_local, 1), (int64_t(1) << 31) / std::max<int64_t>(per_cand, 1))));
+    const int cb = chunk >= 8 ? 8 : (chunk >= 4 ? 4 : (chunk >= 2 ? 2 : 1));
+
+    McParams P{};
+    P.n_slices = static_cast<int32_t>(ns);
+    P.n_quotes = nq;
+    P.max_q = job.max_q;
+    P.n_tiles = n_tiles;
+    P.ppt = ppt;
+    P.rng = plan.rng;
+    P.total_steps = S;
+    P.num_paths = plan.num_paths;
+    P.block_size = plan.block_size;
+    P.seed = plan.seed;
+    P.slices = upload(ctx, "t2_slices", job.slices);
+    P.hdt = upload(ctx, "t2_hdt", job.hdt);
+    P.strikes = upload(ctx, "t2_strikes", surface.K);
+    P.jump = upload(ctx, "t2_jump", jump);
+    const double* d_market = upload(ctx, "t2_market", market);
+    const double* d_tend = upload(ctx, "t2_tend", t_end);
+    const double* d_dt = upload(ctx, "t2_dt", dt);
+    const double* d_sdt = upload(ctx, "t2_sdt", sdt);
+    const size_t nl = static_cast<size_t>(std::max(n_local, 1));
+    auto* chains = static_cast<T2Chain*>(dev_buf(ctx, "t2_chains", sizeof(T2Chain) * nl));
+    auto* alpha0 = static_cast<double*>(dev_buf(ctx, "t2_alpha0", sizeof(double) * nl));
+    auto* beta = static_cast<double*>(dev_buf(ctx, "t2_beta", sizeof(double) * nl));
+    auto* active = static_cast<uint8_t*>(dev_buf(ctx, "t2_active", nl));
+    auto* cost = static_cast<double*>(dev_buf(ctx, "t2_cost", sizeof(double) * nl));
+    auto* bad = static_cast<int*>(dev_buf(ctx, "t2_bad", sizeof(int) * nl));
+    auto* nonfinite = static_cast<int*>(dev_buf(ctx, "t2_nonfinite", sizeof(int)));
+    auto* coef = static_cast<StepCoef*>(dev_buf(ctx, "t2_coef", sizeof(StepCoef) * S * chunk));
+    auto* partials = static_cast<double*>(
+        dev_buf(ctx, "t2_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * n_tiles * chunk));
+    auto* values = static_cast<double*>(dev_buf(ctx, "t2_values", sizeof(double) * static_cast<size_t>(nq) * chunk));
+    check_cuda(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx->stream), "memset");
+    check_cuda(cudaMemsetAsync(bad, 0, sizeof(int) * nl, ctx->stream), "memset");
+
+    // ---- annealer state (device resident) ----
+    sabr_sa_state st{};
+    for (size_t i = 0; i < start_full.size(); ++i) st.incumbent[i] = st.best[i] = start_full[i];
+    st.incumbent_value = st.best_value = start_value;
+    st.evals = 1;
+    st.done = (L == 0 || st.evals >= sch.max_evals) ? 1 : 0;
+    st.eval_cap = st.done ? 0 : (sch.max_evals - st.evals + n_chains - 1) / n_chains;
+
+    SaLevelArgs a{};
+    a.dim_full = 10;
+    a.nranks = ctx->nranks;
+    a.chain_begin = begin;
+    a.n_local = n_local;
+    a.n_chains = n_chains;
+    a.max_evals = sch.max_evals;
+    a.levels_total = L;
+    const int64_t grid = std::max<int64_t>(1, (n_local + sa_block_threads() - 1) / sa_block_threads());
+    a.state = static_cast<sabr_sa_state*>(dev_buf(ctx, "sa_state", sizeof(sabr_sa_state)));
+    a.block_recs = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_block_recs", sizeof(sabr_level_record) * grid));
+    a.rank_rec = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_rank_rec", sizeof(sabr_level_record)));
+    auto* recv = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_recv_recs", sizeof(sabr_level_record) * ctx->nranks));
+    a.ticket = static_cast<unsigned int*>(dev_buf(ctx, "sa_ticket", sizeof(unsigned int)));
+    a.trace_f = static_cast<double*>(dev_buf(ctx, "sa_trace", sizeof(double) * std::max<int64_t>(1, L)));
+    check_cuda(cudaMemcpyAsync(a.state, &st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream), "H2D state");
+    check_cuda(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), ctx->stream), "memset ticket");
+
+    T2StepArgs ta{};
+    for (int i = 0; i < 10; ++i) {
+        ta.lo[i] = ps.defs[i].lo;
+        ta.hi[i] = ps.defs[i].hi;
+        ta.range[i] = ps.defs[i].hi - ps.defs[i].lo;
+    }
+    ta.free_mask = ps.free_mask();
+    ta.n_local = n_local;
+    ta.t0 = sch.t0;
+    ta.horizon = horizon;
+    ta.seed = sch.seed;
+    ta.chain_begin = begin;
+
+    Timer timer(ctx);
+    timer.start();
+    int64_t mc_launches = 0, launches = 0;
+    auto* pinned = static_cast<int64_t*>(ctx->pinned);
+    for (int64_t level = 0; level < L; ++level) {
+        ta.level = level;
+        ta.temp = temps[level];
+        check_cuda(launch_t2_level_init(chains, a.state, ta, ctx->stream), "t2_level_init");
+        for (int step = 0; step < sch.chain_length; ++step) {
+            check_cuda(launch_t2_propose(chains, a.state, ta, alpha0, beta, active, ctx->stream), "t2_propose");
+            for (int32_t c0 = 0; c0 < n_local; c0 += chunk) {
+                const int32_t nc = std::min(chunk, n_local - c0);
+                check_cuda(launch_t2_coef(chains + c0, active + c0, nc, d_tend, d_dt, d_sdt, S, coef,
+                                          ctx->stream), "t2_coef");
+                McParams Q = P;
+                Q.n_cand = nc;
+                Q.alpha0 = alpha0 + c0;
+                Q.beta = beta + c0;
+                Q.active = active + c0;
+                Q.coef = coef;
+                Q.partials = partials;
+                Q.terminals = nullptr;
+                Q.bad = bad + c0;
+                timer.before();
+                check_cuda(launch_mc_tiles(Q, cb, ctx->stream), "mc_tiles");
+                timer.after();
+                check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, cost + c0, ctx->stream), "mc_reduce");
+                mc_launches += 1;
+                launches += 4;
+            }
+            check_cuda(launch_t2_accept(chains, ta, cost, bad, nonfinite, ctx->stream), "t2_accept");
+            launches += 2;
+        }
+        check_cuda(launch_t2_level_end(chains, a, level, ctx->stream), "t2_level_end");
+        if (ctx->nranks > 1) {
+            allgather(ctx, a.rank_rec, recv, sizeof(sabr_level_record));
+            check_cuda(launch_sa_merge(a, recv, level, ctx->stream), "sa_merge");
+        }
+        check_cuda(cudaMemcpyAsync(pinned, &a.state->done, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                   ctx->stream), "D2H done");
+        check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+        if (*pinned) break;
+    }
+    sabr_sa_state out{};
+    int nf = 0;
+    check_cuda(cudaMemcpyAsync(&out, a.state, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
+    check_cuda(cudaMemcpyAsync(&nf, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+    const double evals_run = static_cast<double>(out.evals - 1);
+    timer.stop(evals_run, evals_run * static_cast<double>(plan.num_paths) * static_cast<double>(S),
+               mc_launches, launches);
+    if (nf) fail(SABR_E_RUNTIME, "mc: non-finite path value (scheme unstable for these inputs)");
+
+    AnnealOut r;
+    r.best_full.assign(out.best, out.best + 10);
+    r.best_value = out.best_value;
+    r.evals = out.evals;
+    r.trace_f.resize(out.levels_run);
+    if (out.levels_run > 0)
+        check_cuda(cudaMemcpy(r.trace_f.data(), a.trace_f, sizeof(double) * out.levels_run,
+                              cudaMemcpyDeviceToHost), "D2H trace");
+    r.trace_t.assign(temps.begin(), temps.begin() + out.levels_run);
+    return r;
+}
+
+}  // namespace sabr_gpu

@@ -377,3 +377,25 @@ def ref_parse_surface(path):
     r._check(r.lib.ref_surface_csv_read(path.encode(), C.byref(spot), _dptr(T), _dptr(rr), _dptr(y),
                                         off.ctypes.data_as(C.POINTER(C.c_int64)), _dptr(K), _dptr(v)))
     return VolSurface.from_arrays(spot.value, T, rr, y, off, K, v)
+
+
+def atm_vol_guess(surface, slice):
+    """atm_vol_guess, calibration.cpp:143-153 (alpha start of the calibrators)."""
+    fwd = surface.forward(slice)
+    qs = surface.slices[slice].quotes
+    best, dist = qs[0].vol, abs(qs[0].strike - fwd)
+    for q in qs:
+        if abs(q.strike - fwd) < dist:
+            dist, best = abs(q.strike - fwd), q.vol
+    return best
+
+
+def cost_sensitivity(orc, model, surface, slice, params):
+    """|cost(libm +-1 ulp) - cost| per vector (oracle/sabr_oracle.c)."""
+    orc.lib.orc_cost_sensitivity.restype = C.c_double
+    s, keep = surface.to_abi()
+    dim = 4 if model == A.MODEL_STATIC else 6
+    P = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, dim)
+    return np.array([orc.lib.orc_cost_sensitivity(C.c_int(model), C.byref(s), C.c_int64(slice),
+                                                  _dptr(np.ascontiguousarray(P[i])))
+                     for i in range(P.shape[0])])

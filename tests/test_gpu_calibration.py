@@ -1,0 +1,103 @@
+"""calibrate_* through the C-ABI against the compiled reference's own
+calibrate_* (proj/src/calibration.cpp) and its unit tests
+(proj/tests/test_calibration.cpp)."""
+import numpy as np
+import pytest
+
+import paper_2407_20713_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+
+def c1_schedule(seed):
+    # acceptance.cpp:318-323
+    return pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=seed)
+
+
+def close_reports(g, r, rtol=1e-10):
+    assert g.model == r.model and g.technique == r.technique and g.quantity == r.quantity
+    assert g.evals == r.evals
+    assert abs(g.final_cost - r.final_cost) <= rtol * abs(r.final_cost)
+    assert g.params.keys() == r.params.keys()
+    for k in r.params:
+        assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), (k, g.params[k], r.params[k])
+    assert len(g.rows) == len(r.rows)
+    for a, b in zip(g.rows, r.rows):
+        assert a.maturity == b.maturity and a.strike == b.strike and a.market == b.market
+        assert abs(a.model - b.model) <= 1e-9 * abs(b.model)
+    assert abs(g.mean_rel_error - r.mean_rel_error) <= 1e-7 * r.mean_rel_error
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_static_T1_matches_reference(engine, ref, eq_surface, seed):
+    s = c1_schedule(seed)
+    g = engine.calibrate_static_T1(eq_surface, 0, None, s, None)
+    r = ref.calibrate_static_T1(eq_surface, 0, None, s, None)
+    close_reports(g, r)
+    assert g.seed == seed
+
+
+def test_static_T1_fixed_and_bounds(engine, ref, fx_surface):
+    s = pkg.AnnealingSchedule(t0=1.0, cooling=0.8, chain_length=10, workers=4, t_min=1e-2, seed=1)
+    g = engine.calibrate_static_T1(fx_surface, 0, {"nu": (0.01, 3.0)}, s, {"beta": 0.75, "rho": -0.4})
+    r = ref.calibrate_static_T1(fx_surface, 0, {"nu": (0.01, 3.0)}, s, {"beta": 0.75, "rho": -0.4})
+    close_reports(g, r)
+    assert g.params["beta"] == 0.75 and g.params["rho"] == -0.4
+
+
+def test_evaluation_only_mode(engine, ref, eq_surface):
+    fixed = {"alpha": 0.289271, "beta": 1.0, "nu": 0.308560, "rho": -0.999729}
+    g = engine.calibrate_static_T1(eq_surface, 2, None, pkg.AnnealingSchedule(seed=99), fixed)
+    r = ref.calibrate_static_T1(eq_surface, 2, None, pkg.AnnealingSchedule(seed=99), fixed)
+    assert g.evals == 1 and len(g.rows) == 21
+    close_reports(g, r)
+
+
+def test_case1_T1_matches_reference(engine, ref, fx_surface):
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.9, chain_length=50, workers=32, t_min=1e-5, seed=1)
+    g = engine.calibrate_dynamic_case1_T1(fx_surface, None, s, {"beta": 1.0})
+    r = ref.calibrate_dynamic_case1_T1(fx_surface, None, s, {"beta": 1.0})
+    close_reports(g, r)
+
+
+def test_case1_evaluation_published_fit(engine, ref, eq_surface):
+    p = pkg.CaseIParams(0.294722, 1.0, -1.0, 0.388539, 0.001, 0.131466)
+    g = engine.evaluate_case1(eq_surface, p)
+    assert len(g.rows) == 84 and g.quantity == "vol"
+    assert abs(g.mean_rel_error - 2.073025e-2) <= 2.5e-2 * 2.073025e-2
+    assert g.max_rel_error < 0.10
+    close_reports_eval = ref.evaluate_case1(eq_surface, p)
+    assert abs(g.final_cost - close_reports_eval.final_cost) <= 1e-12 * close_reports_eval.final_cost
+
+
+def test_errors_map_to_reference_exceptions(engine, fx_surface):
+    s = pkg.AnnealingSchedule()
+    with pytest.raises(pkg.DomainError):
+        engine.calibrate_static_T1(fx_surface, 0, {"alpha": (2.0, 1.0)}, s, None)
+    with pytest.raises(pkg.DomainError):
+        engine.calibrate_static_T1(fx_surface, 0, {"gamma": (0.0, 1.0)}, s, None)
+    with pytest.raises(pkg.DomainError):
+        engine.calibrate_static_T1(fx_surface, 0, None, s, {"gamma": 0.5})
+    with pytest.raises(pkg.OutOfRangeError):
+        engine.calibrate_static_T1(fx_surface, 9, None, s, None)
+    one = pkg.VolSurface(fx_surface.spot, [fx_surface.slices[0]])
+    with pytest.raises(pkg.DomainError):
+        engine.calibrate_dynamic_case1_T1(one, None, s, None)
+
+
+def test_case2_T2_matches_reference(engine, ref, eq_surface):
+    """calibrate_case2_T2 end to end (no reference test exists for it: the
+    reference itself is the oracle here).  C4 shape at small scale: the T = 1
+    equity slice, dynamics pinned static, reference xoshiro streams."""
+    surf = pkg.VolSurface(eq_surface.spot, [eq_surface.slices[2]])
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=4, workers=6, t_min=0.2, seed=3)
+    plan = pkg.SimulationPlan(num_paths=2048, seed=1)
+    g = engine.calibrate_case2_T2(surf, None, s, plan, fixed)
+    r = ref.calibrate_case2_T2(surf, None, s, plan, fixed)
+    assert g.evals == r.evals
+    assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
+    for k in r.params:
+        assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
+    for a, b in zip(g.rows, r.rows):
+        assert abs(a.model - b.model) <= 1e-9 * abs(b.model)

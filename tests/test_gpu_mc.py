@@ -1,0 +1,122 @@
+"""GPU log-Euler Monte Carlo vs the reference (proj/src/mc.cpp) and the
+Philox restatement (oracle/sabr_oracle.c).
+
+Tolerances: identical streams in FP64 -> per-path F_T within 1e-12 relative
+(the GPU carries ln F and uses libdevice transcendentals, so paths differ from
+glibc in the last bits), prices within 1e-11 relative.  Statistical pins of
+proj/tests/test_mc.cpp hold with the reference's sigma multiples."""
+import numpy as np
+import pytest
+
+import paper_2407_20713_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+K_STATIC = pkg.StaticSabrParams(0.375162, 0.999999, 0.331441, -0.999999)
+K_CASE1 = pkg.CaseIParams(0.393329, 1.0, -1.0, 0.941565, 0.001, 1.246906)
+K_CASE2 = pkg.CaseIIParams(0.398436, 0.999579, -0.964678, 0.0, 0.101632, 1.285129, 1.302296, -0.086294,
+                           0.0, 2.059560, 0.495890)
+F0, T = 2257.37, 0.495890
+
+
+def plan(n=1 << 15, seed=1, rng="xoshiro", block=4096, dt=1 / 250):
+    return pkg.SimulationPlan(num_paths=n, dt=dt, seed=seed, block_size=block, rng=rng)
+
+
+@pytest.mark.parametrize("params", [K_STATIC, K_CASE1, K_CASE2, pkg.StaticSabrParams(0.3, 0.7, 0.5, -0.4)])
+@pytest.mark.parametrize("block", [4096, 1000, 3])
+def test_terminals_match_reference_streams(engine, ref, params, block):
+    p = plan(n=10_000, seed=3, block=block)
+    g = engine.simulate_terminals(params, F0, params.alpha, T, p)
+    r = ref.simulate_terminals(params, F0, params.alpha, T, p, serial=True)
+    err = np.max(np.abs(g - r) / np.abs(r))
+    assert err < 1e-12, err
+
+
+@pytest.mark.parametrize("params", [K_STATIC, K_CASE1, K_CASE2])
+def test_terminals_match_philox_restatement(engine, orc, params):
+    p = plan(n=5_000, seed=11, rng="philox")
+    g = engine.simulate_terminals(params, F0, params.alpha, T, p)
+    o = orc.simulate_terminals(params, F0, params.alpha, T, p)
+    assert np.max(np.abs(g - o) / np.abs(o)) < 1e-12
+
+
+@pytest.mark.parametrize("rng", ["xoshiro", "philox"])
+def test_prices_match(engine, ref, orc, rng):
+    p = plan(n=1 << 16, seed=6, rng=rng)
+    strikes = [0.8 * F0, 0.9 * F0, F0, 1.1 * F0, 1.2 * F0]
+    g = engine.price_european_batch(K_CASE2, F0, strikes, 0.018196, 0.034516, T, p)
+    w = (ref if rng == "xoshiro" else orc).price_european_batch(K_CASE2, F0, strikes, 0.018196, 0.034516, T, p)
+    for a, b in zip(g, w):
+        assert abs(a.value - b.value) <= 1e-11 * abs(b.value)
+        assert abs(a.std_error - b.std_error) <= 1e-8 * abs(b.std_error)
+
+
+def test_martingale(engine):
+    # test_mc.cpp:26-39
+    terms = engine.simulate_terminals(K_STATIC, F0, K_STATIC.alpha, 0.5, plan(n=1 << 17, seed=5))
+    se = terms.std(ddof=1) / np.sqrt(len(terms))
+    assert abs(terms.mean() - F0) < 4 * se
+
+
+def test_lognormal_limit_matches_black_scholes(engine):
+    # test_mc.cpp:41-54
+    p = pkg.StaticSabrParams(0.25, 1.0, 0.0, 0.0)
+    est = engine.price_european_call(p, 100.0, 105.0, 0.02, 0.01, 1.0, plan(n=1 << 17, seed=2))
+    bs = pkg.black_scholes_call(100.0, 105.0, 0.02, 0.01, 1.0, 0.25)
+    assert abs(est.value - bs) < 3.5 * est.std_error and est.std_error > 0
+
+
+def test_batch_equals_single(engine):
+    # test_mc.cpp:85-100 (bit-for-bit)
+    p = plan(seed=6)
+    strikes = [0.9 * F0, F0, 1.1 * F0]
+    batch = engine.price_european_batch(K_STATIC, F0, strikes, 0.018196, 0.034516, T, p)
+    for k, b in zip(strikes, batch):
+        single = engine.price_european_call(K_STATIC, F0, k, 0.018196, 0.034516, T, p)
+        assert single.value == b.value and single.std_error == b.std_error
+    assert batch[0].value > batch[1].value > batch[2].value
+
+
+def test_case2_zero_terms_bit_identical_to_case1(engine):
+    # test_mc.cpp:102-114
+    c1 = pkg.CaseIParams(0.3, 1.0, -0.6, 0.8, 0.9, 1.7)
+    c2 = pkg.CaseIIParams(0.3, 1.0, -0.6, 0.0, 0.0, 0.8, 0.0, 0.0, 0.9, 1.7, 2.0)
+    p = plan(n=1 << 13, seed=7)
+    a = engine.simulate_terminals(c1, 100.0, 0.3, 1.0, p)
+    b = engine.simulate_terminals(c2, 100.0, 0.3, 1.0, p)
+    assert np.array_equal(a, b)
+
+
+def test_worker_count_does_not_change_results(engine):
+    p1, p8 = plan(seed=4), plan(seed=4)
+    p8.workers = 8
+    a = engine.simulate_terminals(K_CASE1, F0, K_CASE1.alpha, T, p1)
+    b = engine.simulate_terminals(K_CASE1, F0, K_CASE1.alpha, T, p8)
+    assert np.array_equal(a, b)
+
+
+def test_plan_and_model_validation(engine):
+    with pytest.raises(pkg.DomainError):
+        engine.simulate_terminals(K_STATIC, F0, 0.3, T, plan(n=0))
+    with pytest.raises(pkg.DomainError):
+        engine.simulate_terminals(K_STATIC, F0, 0.3, 0.001, plan())  # shorter than one step
+    with pytest.raises(pkg.ConstraintError):
+        bad = pkg.CaseIIParams(0.3, 1.0, -0.9, 0.0, -0.5, 0.5, 0.0, 0.0, 0.1, 0.1, 2.0)
+        engine.simulate_terminals(bad, F0, 0.3, T, plan())
+
+
+def test_published_fx_prices_case2(engine, fx_surface):
+    # acceptance c8 (acceptance.cpp:259-286): 12 published prices within 3 sigma, 2^20 paths, seed 5
+    p = pkg.CaseIIParams(0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807,
+                         0.0, 150.0, 2.0)
+    want = [[0.101712, 0.040476, 0.011697], [0.144950, 0.056139, 0.015539],
+            [0.198897, 0.075409, 0.020010], [0.260539, 0.101766, 0.028189]]
+    worst = 0.0
+    for i, s in enumerate(fx_surface.slices):
+        strikes = [s.quotes[c].strike for c in (3, 9, 15)]
+        est = engine.price_european_batch(p, fx_surface.spot, strikes, s.rate, s.dividend, s.maturity,
+                                          plan(n=1 << 20, seed=5))
+        for j in range(3):
+            worst = max(worst, abs(est[j].value - want[i][j]) / est[j].std_error)
+    assert worst < 3.0, worst
