@@ -51,7 +51,7 @@ def c4_setup(levels=2):
 
     eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
     surf = pkg.VolSurface(eq.spot, [eq.slices[2]])
-    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0}
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
     t_min = 2.0 * 0.96 ** (levels - 1) * 0.999
     sch = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=t_min, seed=1,
                                 max_evals=10 ** 12)

@@ -757,6 +757,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.beta = upload(ctx, "mc_beta", std::vector<double>{beta});
     P.active = nullptr;
     P.coef = upload(ctx, "mc_coef", coef);
+    P.cand_stride = 1;
     P.hdt = upload(ctx, "mc_hdt", job.hdt);
     P.strikes = upload(ctx, "mc_strikes", strikes);
     P.jump = upload(ctx, "mc_jump", jump);
@@ -1050,7 +1051,9 @@ SABR_API sabr_status sabr_calibrate_case2_T2(sabr_ctx* ctx, const sabr_surface* 
             tf = r.trace_f;
         }
         const auto bp = with_h(best_full);
+        const sabr_timing sa_timing = ctx->timing;  // the report's MC run must not replace it
         Report rep = evaluate_case2_impl(ctx, surface, bp.data(), report_plan ? *report_plan : *plan);
+        ctx->timing = sa_timing;
         rep.params = ps.named(best_full);
         rep.final_cost = best_value;
         rep.evals = evals;
@@ -1224,6 +1227,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
         P.alpha0 = upload(ctx, "mc_alpha0", std::vector<double>{alpha0});
         P.beta = upload(ctx, "mc_beta", std::vector<double>{params[1]});
         P.coef = upload(ctx, "mc_coef", coef);
+        P.cand_stride = 1;
         P.hdt = upload(ctx, "mc_hdt", job.hdt);
         P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});
         P.jump = upload(ctx, "mc_jump", jump);

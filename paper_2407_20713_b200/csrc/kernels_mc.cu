@@ -32,7 +32,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <int CB>
-__global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
+__global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_constant__ McParams P) {
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
     int64_t idx = blockIdx.x;
@@ -45,21 +45,25 @@ __global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
     const int mq = sl.q_end - sl.q_begin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    bool act[CB];
-    bool logn[CB];
-    double bm1[CB], a0[CB];
-    int n_act = 0;
+    // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
+    // log space, F = F0 exp(x), alpha = exp(la):
+    //   nu_hat = alpha F^(beta-1) = exp(la + (beta-1)(ln F0 + x))   (mc.cpp:99-100)
+    //   la    += nu z1 sqrt(dt) - nu^2 dt / 2                         (mc.cpp:97-98)
+    //   x     += nu_hat (rho z1 + srho z2) sqrt(dt) - nu_hat^2 dt / 2  (mc.cpp:101-102)
+    // Inactive / padding candidates have zero coefficients and are skipped in
+    // the payoffs: no per-candidate branch in the step loop.
+    uint32_t act_mask = 0, logn_mask = 0;
+    double la0[CB], bm1[CB];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) {
         const int c = c0 + cc;
-        act[cc] = c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
-        n_act += act[cc];
-        const double beta = act[cc] ? P.beta[c] : 1.0;
-        logn[cc] = beta == 1.0;  // mc.cpp:58 fast path
-        bm1[cc] = beta - 1.0;
-        a0[cc] = act[cc] ? (logn[cc] ? P.alpha0[c] : log(P.alpha0[c])) : 0.0;
+        const bool act = c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
+        act_mask |= act ? (1u << cc) : 0u;
+        la0[cc] = act ? log(P.alpha0[c]) : 0.0;
+        bm1[cc] = act ? P.beta[c] - 1.0 : 0.0;
+        logn_mask |= (bm1[cc] == 0.0) ? (1u << cc) : 0u;  // beta == 1: nu_hat = alpha exactly
     }
-    if (n_act == 0) return;
+    if (act_mask == 0) return;
 
     const bool reduce = P.partials != nullptr;
     if (reduce) {
@@ -80,20 +84,23 @@ __global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
         rng.jump(pl);
     }
 
-    const StepCoef* __restrict__ coef = P.coef + sl.step_off;
+    const int64_t cstride = P.cand_stride;
+    const StepCoef* __restrict__ crow0 = P.coef + static_cast<int64_t>(sl.step_off) * cstride + c0;
     const double* __restrict__ hdt = P.hdt + sl.step_off;
+    const double lnf0 = sl.lnf0;
 
     for (int k = 0; k < P.ppt; ++k) {
         const uint64_t path = p0 + k;
         const bool live = path < P.num_paths;
-        double a[CB], x[CB];
+        double la[CB], x[CB];
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {
-            a[cc] = a0[cc];
+            la[cc] = la0[cc];
             x[cc] = 0.0;
         }
         if (live) {
-            for (int i = 0; i < sl.n_steps; ++i) {
+            const StepCoef* crow = crow0;
+            for (int i = 0; i < sl.n_steps; ++i, crow += cstride) {
                 double ua, ub;
                 if (P.rng == SABR_RNG_XOSHIRO) {
                     ua = rng.uniform();
@@ -106,17 +113,14 @@ __global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
                 const double h = __ldg(hdt + i);
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
-                    if (!act[cc]) continue;
-                    const StepCoef q = coef[static_cast<int64_t>(c0 + cc) * P.total_steps + i];
-                    double nh;
-                    if (logn[cc]) {  // nu_hat = alpha (mc.cpp:99-100)
-                        nh = a[cc];
-                        a[cc] *= exp(q.c1 * z1 - q.c2);
-                    } else {          // nu_hat = alpha F^(beta-1), alpha carried as ln alpha
-                        nh = exp(a[cc] + bm1[cc] * (sl.lnf0 + x[cc]));
-                        a[cc] += q.c1 * z1 - q.c2;
-                    }
-                    x[cc] += nh * (q.rs * z1 + q.ss * z2) - nh * nh * h;
+                    const double2 qa = __ldg(reinterpret_cast<const double2*>(crow + cc));
+                    const double2 qb = __ldg(reinterpret_cast<const double2*>(crow + cc) + 1);
+                    const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
+                    const double arg = ((logn_mask >> cc) & 1u) ? la[cc] : fma(bm1[cc], lnf0 + x[cc], la[cc]);
+                    const double nh = exp(arg);
+                    la[cc] += fma(q.x, z1, -q.y);
+                    const double u = fma(q.w, z2, q.z * z1);
+                    x[cc] = fma(nh, fma(-nh, h, u), x[cc]);
                 }
             }
         }
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {
             F[cc] = sl.forward0 * exp(x[cc]);
-            if (live && act[cc] && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);  // mc.cpp:133-138
+            if (live && ((act_mask >> cc) & 1u) && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);  // mc.cpp:133-138
         }
         if (P.terminals != nullptr && live) P.terminals[path] = F[0];
         if (!reduce) continue;
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(kMcThreads) mc_tile_kernel(const McParams P) {
             const double K = __ldg(P.strikes + sl.q_begin + j);
 #pragma unroll
             for (int cc = 0; cc < CB; ++cc) {
-                if (!act[cc]) continue;
+                if (!((act_mask >> cc) & 1u)) continue;
                 const double d = F[cc] - K;
                 const double v = live ? sl.discount * ((d < 0.0) ? 0.0 : d) : 0.0;
                 const double s1 = warp_sum(v);

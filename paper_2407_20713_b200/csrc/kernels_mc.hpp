@@ -41,8 +41,10 @@ struct McParams {
     const McSlice* slices;  // [n_slices]
     const double* alpha0;   // [n_cand]
     const double* beta;     // [n_cand]
-    const uint8_t* active;  // [n_cand] or null: skip inactive candidates
-    const StepCoef* coef;   // [n_cand][total_steps]
+    const uint8_t* active;  // [n_cand] or null: inactive candidates (zero coefficients)
+                            // are simulated harmlessly and skipped in the payoffs
+    int32_t cand_stride;    // candidates per coefficient row (n_cand rounded up to CB)
+    const StepCoef* coef;   // [total_steps][cand_stride] (step-major; padding = 0)
     const double* hdt;      // [total_steps] dt/2
     const double* strikes;  // [n_quotes]
     const uint64_t* jump;   // xoshiro jump polynomials, 4 words each

@@ -48,10 +48,13 @@ __host__ __device__ inline size_t stage_bytes(int ns, int nq) {
 }
 
 // Cooperative copy of the market grid into shared memory ("staged once").
-__device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem, bool use_smem) {
+// SMEM is a compile-time choice so the quote reads compile to LDS (a runtime
+// smem/global choice would force generic LD + 64-bit address arithmetic).
+template <bool SMEM>
+__device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem) {
     Grid g;
     g.ns = sv.n_slices;
-    if (!use_smem) {  // grid too large for shared memory: read through L1
+    if constexpr (!SMEM) {  // grid too large for shared memory: read through L1
         g.T = sv.T;
         g.lnf_hi = sv.lnf_hi;
         g.lnf_lo = sv.lnf_lo;
@@ -146,8 +149,9 @@ __device__ double builtin_value(int id, const double* x) {
     return CUDART_NAN;
 }
 
-template <int KIND>
-__device__ __forceinline__ double objective(const double* v, const Grid& g, int builtin) {
+template <int KIND, int NQ>
+__device__ __forceinline__ double objective(const double* v, const Grid& g, const SurfaceView& sv,
+                                            int builtin) {
     if constexpr (KIND == OBJ_STATIC) return static_cost(v, g);
     else if constexpr (KIND == OBJ_CASE1) return case1_cost(v, g);
     else return builtin_value(builtin, v);
@@ -226,10 +230,15 @@ __device__ void block_reduce(RedShared& rs, ArgMin e, ArgMin b, long long n) {
 }
 
 // --------------------------------------------------------- level kernel ---
-template <int KIND, int DIMF>
-__global__ void __launch_bounds__(kThreads)
-    sa_level_kernel(const SurfaceView sv, const SaLevelArgs a, const int64_t level,
-                    const double temp, const int use_smem) {
+// Min CTAs/SM: 1e5 chains = 782 CTAs of 128 must fit ONE wave on 148 SMs
+// (6 CTAs/SM -> <= 85 registers); Case I carries more live state.
+template <int KIND>
+constexpr int level_min_ctas() { return 6; }
+
+template <int KIND, int DIMF, int NQ, bool SMEM>
+__global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
+    sa_level_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
+                    const int64_t level, const double temp) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared rs;
     __shared__ sabr_level_record rec;
@@ -238,17 +247,21 @@ __global__ void __launch_bounds__(kThreads)
     if (st->done) return;  // early-stopped run (max_evals): uniform exit
 
     Grid g{};
-    if constexpr (KIND != OBJ_BUILTIN) g = stage_grid(sv, smem, use_smem != 0);
+    if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
 
     const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const bool active = local < a.n_local;
     const int64_t chain = a.chain_begin + local;
 
-    double x[DIMF], y[DIMF], bp[DIMF];
+    // the chain-best point is written only on improvement and read once at
+    // the end: it lives in shared memory (column per thread), not registers
+    __shared__ double bp_s[DIMF][kThreads];
+    double* const bp = &bp_s[0][threadIdx.x];  // bp[i * kThreads] = dim i
+    double x[DIMF], y[DIMF];
 #pragma unroll
     for (int i = 0; i < DIMF; ++i) {
         x[i] = st->incumbent[i];
-        bp[i] = x[i];
+        bp[i * kThreads] = x[i];
     }
     double fx = st->incumbent_value;
     double bv = fx;
@@ -279,7 +292,7 @@ __global__ void __launch_bounds__(kThreads)
                 }
             }
             if (!predicate_ok(a.predicate, y)) continue;  // annealer.cpp:122
-            double fy = objective<KIND>(y, g, a.builtin);
+            double fy = objective<KIND, NQ>(y, g, sv, a.builtin);
             if (isnan(fy)) fy = CUDART_INF;  // safe_eval, annealer.cpp:84-87
             ++ev;
             // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx)
@@ -292,7 +305,7 @@ __global__ void __launch_bounds__(kThreads)
                 if (fx < bv) {
                     bv = fx;
 #pragma unroll
-                    for (int i = 0; i < DIMF; ++i) bp[i] = x[i];
+                    for (int i = 0; i < DIMF; ++i) bp[i * kThreads] = x[i];
                 }
             }
         }
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (active && chain == rs.b_win.i) {
 #pragma unroll
-        for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp[i];
+        for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp[i * kThreads];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -369,40 +382,41 @@ __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* re
                 a.trace_f + level);
 }
 
-template <int KIND, int DIMF>
-__global__ void sa_start_kernel(const SurfaceView sv, const SaLevelArgs a, const int use_smem) {
+template <int KIND, int DIMF, int NQ, bool SMEM>
+__global__ void sa_start_kernel(const __grid_constant__ SurfaceView sv, const SaLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     Grid g{};
-    if constexpr (KIND != OBJ_BUILTIN) g = stage_grid(sv, smem, use_smem != 0);
+    if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
     if (threadIdx.x != 0) return;
     double x[DIMF];
     for (int i = 0; i < DIMF; ++i) x[i] = a.state->incumbent[i];
-    double v = objective<KIND>(x, g, a.builtin);
+    double v = objective<KIND, NQ>(x, g, sv, a.builtin);
     if (isnan(v)) v = CUDART_INF;
     a.state->incumbent_value = v;
     a.state->best_value = v;
 }
 
-template <int KIND, int DIMF>
+template <int KIND, int DIMF, int NQ, bool SMEM>
 __global__ void __launch_bounds__(kThreads)
-    cost_batch_kernel(const SurfaceView sv, const double* __restrict__ params, const int64_t n,
-                      double* __restrict__ cost, const int use_smem) {
+    cost_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
+                      const int64_t n, double* __restrict__ cost) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const Grid g = stage_grid(sv, smem, use_smem != 0);
+    Grid g{};
+    if constexpr (NQ == 0) g = stage_grid<SMEM>(sv, smem);
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     if (i >= n) return;
     double v[DIMF];
 #pragma unroll
     for (int k = 0; k < DIMF; ++k) v[k] = params[i * DIMF + k];
-    cost[i] = objective<KIND>(v, g, 0);
+    cost[i] = objective<KIND, NQ>(v, g, sv, 0);
 }
 
 // Model vols for every quote of the view (report rows, calibration.cpp:180-194).
-template <int KIND, int DIMF>
-__global__ void vol_batch_kernel(const SurfaceView sv, const double* __restrict__ params,
-                                 const int64_t n, double* __restrict__ vols, const int use_smem) {
+template <int KIND, int DIMF, bool SMEM>
+__global__ void vol_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
+                                 const int64_t n, double* __restrict__ vols) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const Grid g = stage_grid(sv, smem, use_smem != 0);
+    const Grid g = stage_grid<SMEM>(sv, smem);
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double v[DIMF];
@@ -511,15 +525,21 @@ __global__ void t2_propose_kernel(T2Chain* __restrict__ chains, const sabr_sa_st
     beta[c] = y[1];
 }
 
+// coef[i][c] (step-major, cand_stride columns); inactive and padding
+// candidates get zero coefficients (simulated harmlessly, never priced).
 __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t* __restrict__ active,
-                               const int32_t n_local, const double* __restrict__ t_end,
-                               const double* __restrict__ dt, const double* __restrict__ sdt,
-                               const int64_t total_steps, double4* __restrict__ coef) {
+                               const int32_t n_local, const int32_t cand_stride,
+                               const double* __restrict__ t_end, const double* __restrict__ dt,
+                               const double* __restrict__ sdt, const int64_t total_steps,
+                               double4* __restrict__ coef) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= static_cast<int64_t>(n_local) * total_steps) return;
-    const int c = static_cast<int>(t / total_steps);
-    const int64_t i = t % total_steps;
-    if (!active[c]) return;
+    if (t >= static_cast<int64_t>(cand_stride) * total_steps) return;
+    const int c = static_cast<int>(t % cand_stride);
+    const int64_t i = t / cand_stride;
+    if (c >= n_local || !active[c]) {
+        coef[t] = make_double4(0.0, 0.0, 0.0, 0.0);
+        return;
+    }
     const T2Chain& ch = chains[c];
     double p[11];
     for (int k = 0; k < 10; ++k) p[k] = ch.y[k];
@@ -639,27 +659,83 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaSuccess;
 }
 
+// Launch `body(kernel_ptr, smem_bytes)` for the SMEM variant the view
+// supports: the market grid staged in shared memory, or (too large) read
+// through L1.  (Kernel-parameter/constant-bank grids were tried: sm_100a FP64
+// instructions take no constant-bank operands, so they only add registers.)
+template <int KIND, int DIMF, template <int, int, int, bool> class KSel, class Body>
+cudaError_t dispatch_grid(const SurfaceView& sv, Body&& body) {
+    if constexpr (KIND == OBJ_BUILTIN) {
+        return body(KSel<KIND, DIMF, 0, true>::get(), size_t(0));
+    } else {
+        int use = 0;
+        const size_t smem = smem_for(sv, &use);
+        if (use) return body(KSel<KIND, DIMF, 0, true>::get(), smem);
+        return body(KSel<KIND, DIMF, 0, false>::get(), size_t(0));
+    }
+}
+
+template <int K, int D, int N, bool S>
+struct LevelSel {
+    static auto get() { return sa_level_kernel<K, D, N, S>; }
+};
+template <int K, int D, int N, bool S>
+struct StartSel {
+    static auto get() { return sa_start_kernel<K, D, N, S>; }
+};
+template <int K, int D, int N, bool S>
+struct CostSel {
+    static auto get() { return cost_batch_kernel<K, D, N, S>; }
+};
+
 template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
-    int use = 0;
-    const size_t smem = KIND == OBJ_BUILTIN ? 0 : smem_for(sv, &use);
-    auto k = sa_level_kernel<KIND, DIMF>;
-    cudaError_t e = set_smem(k, smem);
-    if (e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>((a.n_local + kThreads - 1) / kThreads);
-    k<<<grid, kThreads, smem, s>>>(sv, a, level, temp, use);
-    return cudaGetLastError();
+    return dispatch_grid<KIND, DIMF, LevelSel>(sv, [&](auto k, size_t smem) {
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kThreads, smem, s>>>(sv, a, level, temp);
+        return cudaGetLastError();
+    });
 }
 
 template <int KIND, int DIMF>
 cudaError_t start_t(const SurfaceView& sv, const SaLevelArgs& a, cudaStream_t s) {
+    return dispatch_grid<KIND, DIMF, StartSel>(sv, [&](auto k, size_t smem) {
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<1, 32, smem, s>>>(sv, a);
+        return cudaGetLastError();
+    });
+}
+
+template <int KIND, int DIMF>
+cudaError_t cost_t(const SurfaceView& sv, const double* params, int64_t n, double* cost,
+                   cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
+    return dispatch_grid<KIND, DIMF, CostSel>(sv, [&](auto k, size_t smem) {
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost);
+        return cudaGetLastError();
+    });
+}
+
+template <int KIND, int DIMF>
+cudaError_t vol_t(const SurfaceView& sv, const double* params, int64_t n, double* vols,
+                  cudaStream_t s) {
     int use = 0;
-    const size_t smem = KIND == OBJ_BUILTIN ? 0 : smem_for(sv, &use);
-    auto k = sa_start_kernel<KIND, DIMF>;
-    cudaError_t e = set_smem(k, smem);
-    if (e != cudaSuccess) return e;
-    k<<<1, 32, smem, s>>>(sv, a, use);
+    const size_t smem = smem_for(sv, &use);
+    const unsigned grid = static_cast<unsigned>((n + 63) / 64);
+    if (use) {
+        auto k = vol_batch_kernel<KIND, DIMF, true>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<grid, 64, smem, s>>>(sv, params, n, vols);
+    } else {
+        vol_batch_kernel<KIND, DIMF, false><<<grid, 64, 0, s>>>(sv, params, n, vols);
+    }
     return cudaGetLastError();
 }
 
@@ -702,44 +778,18 @@ cudaError_t launch_sa_merge(const SaLevelArgs& a, const sabr_level_record* recs,
 
 cudaError_t launch_cost_batch(int kind, const SurfaceView& sv, const double* params,
                               int32_t dim_full, int64_t n, double* cost, cudaStream_t s) {
-    int use = 0;
-    const size_t smem = smem_for(sv, &use);
-    const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
-    if (kind == OBJ_STATIC && dim_full == 4) {
-        auto k = cost_batch_kernel<OBJ_STATIC, 4>;
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost, use);
-    } else if (kind == OBJ_CASE1 && dim_full == 6) {
-        auto k = cost_batch_kernel<OBJ_CASE1, 6>;
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost, use);
-    } else {
-        return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
+    if (n <= 0) return cudaSuccess;
+    if (kind == OBJ_STATIC && dim_full == 4) return cost_t<OBJ_STATIC, 4>(sv, params, n, cost, s);
+    if (kind == OBJ_CASE1 && dim_full == 6) return cost_t<OBJ_CASE1, 6>(sv, params, n, cost, s);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_vol_batch(int kind, const SurfaceView& sv, const double* params,
                              int32_t dim_full, int64_t n, double* vols, cudaStream_t s) {
-    int use = 0;
-    const size_t smem = smem_for(sv, &use);
-    const unsigned grid = static_cast<unsigned>((n + 63) / 64);
-    if (kind == OBJ_STATIC && dim_full == 4) {
-        auto k = vol_batch_kernel<OBJ_STATIC, 4>;
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, 64, smem, s>>>(sv, params, n, vols, use);
-    } else if (kind == OBJ_CASE1 && dim_full == 6) {
-        auto k = vol_batch_kernel<OBJ_CASE1, 6>;
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, 64, smem, s>>>(sv, params, n, vols, use);
-    } else {
-        return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
+    if (n <= 0) return cudaSuccess;
+    if (kind == OBJ_STATIC && dim_full == 4) return vol_t<OBJ_STATIC, 4>(sv, params, n, vols, s);
+    if (kind == OBJ_CASE1 && dim_full == 6) return vol_t<OBJ_CASE1, 6>(sv, params, n, vols, s);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_case2_feasible(const double* params, int64_t n, uint8_t* out, cudaStream_t s) {
@@ -763,12 +813,12 @@ cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2
 }
 
 cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
-                           const double* t_end, const double* dt, const double* sdt,
-                           int64_t total_steps, void* coef, cudaStream_t s) {
-    const int64_t n = static_cast<int64_t>(n_local) * total_steps;
+                           int32_t cand_stride, const double* t_end, const double* dt,
+                           const double* sdt, int64_t total_steps, void* coef, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(cand_stride) * total_steps;
     if (n <= 0) return cudaSuccess;
     t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        chains, active, n_local, t_end, dt, sdt, total_steps, static_cast<double4*>(coef));
+        chains, active, n_local, cand_stride, t_end, dt, sdt, total_steps, static_cast<double4*>(coef));
     return cudaGetLastError();
 }
 

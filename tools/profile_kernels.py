@@ -28,7 +28,7 @@ def main(mode):
         r = eng.calibrate_dynamic_case1_T1(fx, None, s, {"beta": 1.0})
     elif mode == "t2":
         surf = pkg.VolSurface(eq.spot, [eq.slices[2]])
-        fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0}
+        fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
         s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=3, workers=32, t_min=1.5, seed=1)
         plan = pkg.SimulationPlan(num_paths=100_000, seed=1, rng=os.environ.get("SABR_RNG", "xoshiro"))
         r = eng.calibrate_case2_T2(surf, None, s, plan, fixed)
