@@ -503,6 +503,59 @@ int orc_minimize_builtin(int objective, int predicate, const double* lo, const d
                         NULL, lo, hi, dim, sch, start, res);
 }
 
+double orc_builtin_value(int objective, const double* x) {
+    int id = objective;
+    return builtin_obj(x, &id);
+}
+
+/* Chains [chain_begin, chain_end) of one level, reduced with the reference's
+ * scan order (strict '<', lowest chain first) into one record. */
+int orc_level_record(int objective, int predicate, const double* lo, const double* hi, int dim,
+                     const sabr_schedule* sch, const sabr_sa_state* st, uint64_t level,
+                     double temp, int64_t chain_begin, int64_t chain_end,
+                     sabr_level_record* out) {
+    int id = objective;
+    double x[SABR_MAX_DIM], y[SABR_MAX_DIM], bp[SABR_MAX_DIM];
+    memset(out, 0, sizeof(*out));
+    out->end_chain = out->best_chain = -1;
+    for (int64_t chain = chain_begin; chain < chain_end; ++chain) {
+        orc_xoshiro rng;
+        orc_xoshiro_init(&rng, sch->seed, (level << 20) ^ (uint64_t)chain);
+        memcpy(x, st->incumbent, sizeof(double) * dim);
+        memcpy(bp, st->incumbent, sizeof(double) * dim);
+        double fx = st->incumbent_value, bv = st->incumbent_value;
+        long evals = 0;
+        for (int step = 0; step < sch->chain_length; ++step) {
+            if (evals >= st->eval_cap) break;
+            propose(x, y, dim, temp, lo, hi, sch->t0, &rng);
+            if (predicate == SABR_PRED_SUM_LE_1 && !(y[0] + y[1] <= 1.0)) continue;
+            const double raw = builtin_obj(y, &id);
+            const double fy = isnan(raw) ? INFINITY : raw;
+            ++evals;
+            if (fy <= fx || orc_xoshiro_uniform(&rng) < exp(-(fy - fx) / temp)) {
+                memcpy(x, y, sizeof(double) * dim);
+                fx = fy;
+                if (fx < bv) {
+                    bv = fx;
+                    memcpy(bp, x, sizeof(double) * dim);
+                }
+            }
+        }
+        if (out->end_chain < 0 || fx < out->end_value) {
+            out->end_chain = chain;
+            out->end_value = fx;
+            memcpy(out->end_point, x, sizeof(double) * dim);
+        }
+        if (out->best_chain < 0 || bv < out->best_value) {
+            out->best_chain = chain;
+            out->best_value = bv;
+            memcpy(out->best_point, bp, sizeof(double) * dim);
+        }
+        out->evals += evals;
+    }
+    return SABR_OK;
+}
+
 /* --------------------------------------------------------- Monte Carlo --- */
 
 typedef struct {

@@ -64,6 +64,16 @@ int orc_minimize_builtin(int objective, int predicate, const double* lo, const d
                          int dim, const sabr_schedule* sch, const double* start,
                          sabr_anneal_result* res);
 
+/* One temperature level of chains [chain_begin, chain_end) from `st`
+ * (annealer.cpp:107-139) reduced to one record (the per-rank half of
+ * annealer.cpp:141-159): the multi-rank decomposition the GPU engine uses.
+ * objective: a sabr_builtin_objective; returns SABR_OK. */
+int orc_level_record(int objective, int predicate, const double* lo, const double* hi, int dim,
+                     const sabr_schedule* sch, const sabr_sa_state* st, uint64_t level,
+                     double temp, int64_t chain_begin, int64_t chain_end,
+                     sabr_level_record* out);
+double orc_builtin_value(int objective, const double* x);
+
 /* Monte Carlo (proj/src/mc.cpp:30-273).  model/params as in sabr_b200.h. */
 int orc_simulate_terminals(int model, const double* params, double forward0, double alpha0,
                            double T, const sabr_plan* plan, double* out);
