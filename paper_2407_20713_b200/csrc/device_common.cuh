@@ -117,6 +117,43 @@ SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, dou
     ub = static_cast<double>(b >> 11) * 0x1.0p-53;
 }
 
+// ------------------------------------------------------------ fast exp ---
+// exp(x) = 2^(k/128) * e^r, |r| <= ln2/256: k from one FMA with the 1.5*2^52
+// shift trick, 2^(i/128) from a 128-entry double-double table (i = k mod 128,
+// staged in shared memory by the caller), e^r - 1 by a degree-5 polynomial
+// (truncation < 6e-19), 2^(k>>7) applied by an integer add to the exponent.
+// ~0.51 ulp like glibc's exp; 11 FP64 ops and 5 64-bit constants instead of
+// libdevice's 16 FP64 ops and ~11 materialised constants.  Branch-free (a
+// branch would give every inlined call its own reconvergence region and stop
+// the scheduler interleaving independent exps): |x| > 700 saturates to
+// +inf / +0 (exp(700) = 1e304 only feeds non-finite detection), NaN -> NaN.
+// table entry i = {RN(2^(i/128)), RN(2^(i/128) - hi)}: built on the host in
+// long double (kernels_mc.cu: exp_table_host()).
+constexpr int kExpTableSize = 128;
+
+SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
+    constexpr double kInvLn2N = 0x1.71547652b82fep7;  // 128 / ln 2
+    constexpr double kShift = 0x1.8p52;
+    constexpr double kLn2NHi = 0x1.62e42fefa39efp-8;  // ln2/128 = hi + lo (FMA reduction)
+    constexpr double kLn2NLo = 0x1.abc9e3b39803fp-63;
+    const double z = fma(x, kInvLn2N, kShift);
+    const double kd = z - kShift;
+    const int k = static_cast<int>(__double2loint(z));
+    double r = fma(kd, -kLn2NHi, x);
+    r = fma(kd, -kLn2NLo, r);
+    // e^r - 1 = r + r^2/2 + r^3/6 + r^4/24 + r^5/120
+    const double r2 = r * r;
+    const double q = fma(fma(r, 1.0 / 120, 1.0 / 24), r2, fma(r, 1.0 / 6, 0.5));
+    const double p = fma(q, r2, r);
+    const double2 t = tab[k & 127];
+    const double v = t.x + fma(t.x, p, t.y);
+    // scale by 2^(k >> 7): add to the exponent field (result stays normal for |x| <= 700)
+    const double res = __hiloint2double(__double2hiint(v) + ((k >> 7) << 20), __double2loint(v));
+    // NaN fails the test and flows through the arithmetic into res
+    const double sat = x > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
+    return fabs(x) > 700.0 ? sat : res;
+}
+
 // Box-Muller on two uniforms, proj/src/mc.cpp:30-36.  theta = 2*pi*u2 is
 // evaluated as sincospi(2*u2) (2*u2 is exact), i.e. without the rounding of
 // the 2*pi product; differences are below 1e-15 absolute in z.
@@ -236,13 +273,28 @@ struct SmileTerms {
     double c0, a1, a2, inv_omega;
 };
 
+// 1/x for positive, finite, normal x: MUFU.RCP64H seed + two Newton steps
+// (<= 1 ulp; branch-free, unlike the IEEE division's special-case path).
+SABR_HD double fast_rcp(double x) {
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+#else
+    return 1.0 / x;
+#endif
+}
+
 // static_implied_vol, analytics.cpp:183-205 (everything that does not depend
 // on the strike).  pw = pow(f, 1-beta).
 SABR_HD SmileTerms static_terms(double alpha, double beta, double nu, double rho, double pw,
                                 double T) {
     const double one_m_beta = 1.0 - beta;
-    const double omega = pw / alpha;
-    const double inv_omega = 1.0 / omega;
+    const double omega = pw * fast_rcp(alpha);
+    const double inv_omega = alpha * fast_rcp(pw);
     const double rnw = rho * nu * omega;
     const double nw = nu * omega;
     const double rr = 2.0 - 3.0 * rho * rho;
@@ -260,8 +312,8 @@ SABR_HD SmileTerms static_terms(double alpha, double beta, double nu, double rho
 SABR_HD SmileTerms dynamic_terms(double nu1_sq, double nu2_sq, double eta1, double eta2_sq,
                                  double alpha, double beta, double pw, double T) {
     const double one_m_beta = 1.0 - beta;
-    const double omega = pw / alpha;
-    const double inv_omega = 1.0 / omega;
+    const double omega = pw * fast_rcp(alpha);
+    const double inv_omega = alpha * fast_rcp(pw);
     const double e1w = eta1 * omega;
     SmileTerms t;
     t.a1 = 0.5 * (beta - 1.0) + 0.5 * e1w;

@@ -479,6 +479,13 @@ void check_cuda(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(SABR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+const double2* exp_table_device(sabr_ctx* ctx) {
+    auto it = ctx->bufs.find("exptab");
+    if (it != ctx->bufs.end()) return static_cast<const double2*>(it->second.first);
+    const double2* host = exp_table_host();
+    return upload(ctx, "exptab", std::vector<double2>(host, host + sabr_dev::kExpTableSize));
+}
+
 void* dev_buf(sabr_ctx* ctx, const std::string& key, size_t bytes) {
     auto& slot = ctx->bufs[key];
     if (slot.second < bytes) {
@@ -588,6 +595,7 @@ SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& 
     v.lnf_hi = v.T + ns;
     v.lnf_lo = v.T + 2 * ns;
     v.qoff = dq;
+    v.exptab = exp_table_device(ctx);
     return v;
 }
 
@@ -761,6 +769,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.hdt = upload(ctx, "mc_hdt", job.hdt);
     P.strikes = upload(ctx, "mc_strikes", strikes);
     P.jump = upload(ctx, "mc_jump", jump);
+    P.exptab = exp_table_device(ctx);
     P.partials = static_cast<double*>(
         dev_buf(ctx, "mc_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * P.n_tiles));
     P.terminals = nullptr;
@@ -1231,6 +1240,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
         P.hdt = upload(ctx, "mc_hdt", job.hdt);
         P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});
         P.jump = upload(ctx, "mc_jump", jump);
+        P.exptab = exp_table_device(ctx);
         P.partials = nullptr;
         P.terminals = static_cast<double*>(dev_buf(ctx, "mc_terminals", sizeof(double) * plan->num_paths));
         P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
@@ -1291,7 +1301,8 @@ SABR_API sabr_status sabr_minimize_builtin(sabr_ctx* ctx, int32_t objective, int
         validate_schedule(*schedule);
         if (dim < 1 || dim > 4) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
         std::vector<double> lo(lower, lower + dim), hi(upper, upper + dim), st(start, start + dim);
-        const SurfaceView sv{};
+        SurfaceView sv{};
+        sv.exptab = exp_table_device(ctx);
         const T1Out r = run_sa_t1(ctx, OBJ_BUILTIN, sv, static_cast<int>(dim), (1u << dim) - 1u, lo, hi, st,
                                   *schedule, objective, predicate);
         for (int64_t i = 0; i < dim; ++i) result->best_point[i] = r.best_full[i];

@@ -50,6 +50,9 @@ T* upload(sabr_ctx* ctx, const std::string& key, const std::vector<T>& v) {
     return d;
 }
 
+// The exp_tab table (kernels_mc.cu) uploaded once per context.
+const double2* exp_table_device(sabr_ctx* ctx);
+
 // Device view of (part of) a surface; market = per-quote market values
 // (null -> the quoted vols).
 SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& s,

@@ -20,6 +20,7 @@ struct SurfaceView {
     // [n_quotes] x {lm = ln(K/f) (std::log(strike/forward), the reference
     // expression, evaluated on the host), lm*lm, market value, 1/market}
     const double* quotes;
+    const double2* exptab;  // [128] exp_tab table (device_common.cuh), staged per CTA
 };
 
 enum ObjectiveKind : int32_t {

@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     const int c0 = g * CB;
     const int mq = sl.q_end - sl.q_begin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double2 tab[kExpTableSize];
+    for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
 
     // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
     // log space, F = F0 exp(x), alpha = exp(la):
@@ -63,7 +65,8 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
         bm1[cc] = act ? P.beta[c] - 1.0 : 0.0;
         logn_mask |= (bm1[cc] == 0.0) ? (1u << cc) : 0u;  // beta == 1: nu_hat = alpha exactly
     }
-    if (act_mask == 0) return;
+    if (act_mask == 0) return;  // block-uniform
+    __syncthreads();            // exp table staged
 
     const bool reduce = P.partials != nullptr;
     if (reduce) {
@@ -99,8 +102,8 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
             x[cc] = 0.0;
         }
         if (live) {
-            const StepCoef* crow = crow0;
-            for (int i = 0; i < sl.n_steps; ++i, crow += cstride) {
+            // normals of step i (box_muller, mc.cpp:30-36) from the path's stream
+            auto normals = [&](int i, double& z1, double& z2) {
                 double ua, ub;
                 if (P.rng == SABR_RNG_XOSHIRO) {
                     ua = rng.uniform();
@@ -108,26 +111,44 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
                 } else {
                     philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
                 }
-                double z1, z2;
                 box_muller(ua, ub, z1, z2);
+            };
+            // all candidates' log-Euler step i with the shared normals
+            auto advance_all = [&](int i, const StepCoef* crow, double z1, double z2) {
                 const double h = __ldg(hdt + i);
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
                     const double2 qa = __ldg(reinterpret_cast<const double2*>(crow + cc));
                     const double2 qb = __ldg(reinterpret_cast<const double2*>(crow + cc) + 1);
-                    const double4 q = make_double4(qa.x, qa.y, qb.x, qb.y);
                     const double arg = ((logn_mask >> cc) & 1u) ? la[cc] : fma(bm1[cc], lnf0 + x[cc], la[cc]);
-                    const double nh = exp(arg);
-                    la[cc] += fma(q.x, z1, -q.y);
-                    const double u = fma(q.w, z2, q.z * z1);
+                    const double nh = exp_tab(arg, tab);
+                    la[cc] += fma(qa.x, z1, -qa.y);
+                    const double u = fma(qb.y, z2, qb.x * z1);
                     x[cc] = fma(nh, fma(-nh, h, u), x[cc]);
                 }
+            };
+            // software pipeline: the (serial) Box-Muller chain of step i+1 is
+            // independent of the candidate updates of step i, so both sit in
+            // one basic block; the draw order is the reference's (2 per step)
+            // and the last step is peeled so consecutive paths of a thread
+            // continue the block stream exactly.
+            double z1, z2;
+            normals(0, z1, z2);
+            const StepCoef* crow = crow0;
+            const int n = sl.n_steps;
+            for (int i = 0; i + 1 < n; ++i, crow += cstride) {
+                double n1, n2;
+                normals(i + 1, n1, n2);
+                advance_all(i, crow, z1, z2);
+                z1 = n1;
+                z2 = n2;
             }
+            advance_all(n - 1, crow, z1, z2);
         }
         double F[CB];
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {
-            F[cc] = sl.forward0 * exp(x[cc]);
+            F[cc] = sl.forward0 * exp_tab(x[cc], tab);
             if (live && ((act_mask >> cc) & 1u) && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);  // mc.cpp:133-138
         }
         if (P.terminals != nullptr && live) P.terminals[path] = F[0];
@@ -230,6 +251,22 @@ cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s) {
         case 8: return tiles_t<8>(p, s);
     }
     return cudaErrorInvalidValue;
+}
+
+// {RN(2^(i/128)), RN(2^(i/128) - hi)} from x86 long double (64-bit mantissa):
+// the table behind exp_tab, accurate to ~2^-64 relative.
+const double2* exp_table_host() {
+    static double2 table[kExpTableSize];
+    static bool built = false;
+    if (!built) {
+        for (int i = 0; i < kExpTableSize; ++i) {
+            const long double v = exp2l(static_cast<long double>(i) / kExpTableSize);
+            const double hi = static_cast<double>(v);
+            table[i] = make_double2(hi, static_cast<double>(v - static_cast<long double>(hi)));
+        }
+        built = true;
+    }
+    return table;
 }
 
 cudaError_t launch_mc_reduce(const McParams& p, double* value, double* std_error,

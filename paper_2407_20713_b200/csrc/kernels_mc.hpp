@@ -51,7 +51,11 @@ struct McParams {
     double* partials;       // [n_cand][n_quotes][n_tiles][2] (sum, sum of squares) or null
     double* terminals;      // [num_paths] (n_cand == 1, n_slices == 1) or null
     int* bad;               // [n_cand] non-finite flag
+    const double2* exptab;  // [128] 2^(i/128) double-double (exp_tab, device_common.cuh)
 };
+
+// The exp_tab table, built once on the host in long double.
+const double2* exp_table_host();
 
 constexpr int kMcThreads = 128;
 

@@ -40,7 +40,14 @@ struct Grid {
     const double* lnf_lo;
     const int32_t* qoff;
     const Quote* q;
+    const double2* tab;  // exp_tab table in shared memory
 };
+
+// Every kernel stages the 2 KB exp table into shared memory (stage_exp +
+// __syncthreads) before the first exp_tab.
+__device__ __forceinline__ void stage_exp(const SurfaceView& sv, double2* tab_s) {
+    for (int i = threadIdx.x; i < kExpTableSize; i += blockDim.x) tab_s[i] = sv.exptab[i];
+}
 
 __host__ __device__ inline size_t stage_bytes(int ns, int nq) {
     return static_cast<size_t>(nq) * sizeof(Quote) + 3 * sizeof(double) * ns +
@@ -84,31 +91,47 @@ __device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem) {
 
 // f^(1-beta) = exp((1-beta) ln f) with ln f carried in double-double, so the
 // result is as accurate as a correctly rounded exp (pow in analytics.cpp:191).
-__device__ __forceinline__ double pow_fwd(double omb, double lnf_hi, double lnf_lo) {
+__device__ __forceinline__ double pow_fwd(double omb, double lnf_hi, double lnf_lo,
+                                          const double2* tab) {
     const double y = omb * lnf_hi;
     const double err = fma(omb, lnf_hi, -y) + omb * lnf_lo;
-    const double e = exp(y);
+    const double e = exp_tab(y, tab);
     return fma(e, err, e);
 }
 
+__device__ __forceinline__ double quote_rel(const SmileTerms& t, const Quote& qq) {
+    const double sigma = smile_vol(t, qq.lm, qq.lm2);
+    return (qq.mkt - sigma) * qq.inv_mkt;
+}
+
 // Sum of squared relative errors over one slice, calibration.cpp:253-267.
+// Four interleaved partial sums (quotes j mod 4) break the serial FMA chain
+// of the reference's left-to-right sum: the dependency latency of a single
+// accumulator was the kernel's top stall; the reassociation moves the result
+// by ~1 ulp of the cost.
 __device__ __forceinline__ double slice_cost(const SmileTerms& t, const Quote* q, int q0,
                                              int q1) {
-    double sum = 0.0;
-#pragma unroll 4
-    for (int j = q0; j < q1; ++j) {
-        const Quote qq = q[j];
-        const double sigma = smile_vol(t, qq.lm, qq.lm2);
-        const double rel = (qq.mkt - sigma) * qq.inv_mkt;
-        sum = fma(rel, rel, sum);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = q0;
+    for (; j + 4 <= q1; j += 4) {
+        const double r0 = quote_rel(t, q[j]), r1 = quote_rel(t, q[j + 1]);
+        const double r2 = quote_rel(t, q[j + 2]), r3 = quote_rel(t, q[j + 3]);
+        s0 = fma(r0, r0, s0);
+        s1 = fma(r1, r1, s1);
+        s2 = fma(r2, r2, s2);
+        s3 = fma(r3, r3, s3);
     }
-    return sum;
+    for (; j < q1; ++j) {
+        const double r = quote_rel(t, q[j]);
+        s0 = fma(r, r, s0);
+    }
+    return (s0 + s1) + (s2 + s3);
 }
 
 // Objective of calibrate_static_T1: full vector {alpha, beta, nu, rho} on the
 // (single) slice of the view.  calibration.cpp:300-306, analytics.cpp:183-205.
 __device__ __forceinline__ double static_cost(const double* v, const Grid& g) {
-    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0]);
+    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
     const SmileTerms t = static_terms(v[0], v[1], v[2], v[3], pw, g.T[0]);
     return slice_cost(t, g.q, g.qoff[0], g.qoff[1]);
 }
@@ -122,7 +145,7 @@ __device__ __forceinline__ double case1_cost(const double* v, const Grid& g) {
         const double T = g.T[i];
         double n1, n2, e1, e2;
         dyn_coeffs_case1(v[2], v[3], v[4], v[5], T, n1, n2, e1, e2);
-        const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i]);
+        const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
         const SmileTerms t = dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, T);
         sum += slice_cost(t, g.q, g.qoff[i], g.qoff[i + 1]);
     }
@@ -243,11 +266,16 @@ __global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
     __shared__ RedShared rs;
     __shared__ sabr_level_record rec;
 
+    __shared__ double2 tab_s[kExpTableSize];
+
     sabr_sa_state* st = a.state;
     if (st->done) return;  // early-stopped run (max_evals): uniform exit
 
+    stage_exp(sv, tab_s);
     Grid g{};
     if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
 
     const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const bool active = local < a.n_local;
@@ -297,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
             ++ev;
             // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx)
             bool accept = fy <= fx;
-            if (!accept) accept = rng.uniform() < exp(-(fy - fx) / temp);
+            if (!accept) accept = rng.uniform() < exp_tab(-(fy - fx) / temp, tab_s);
             if (accept) {
 #pragma unroll
                 for (int i = 0; i < DIMF; ++i) x[i] = y[i];
@@ -385,8 +413,12 @@ __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* re
 template <int KIND, int DIMF, int NQ, bool SMEM>
 __global__ void sa_start_kernel(const __grid_constant__ SurfaceView sv, const SaLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double2 tab_s[kExpTableSize];
+    stage_exp(sv, tab_s);
     Grid g{};
     if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
     if (threadIdx.x != 0) return;
     double x[DIMF];
     for (int i = 0; i < DIMF; ++i) x[i] = a.state->incumbent[i];
@@ -401,8 +433,12 @@ __global__ void __launch_bounds__(kThreads)
     cost_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
                       const int64_t n, double* __restrict__ cost) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double2 tab_s[kExpTableSize];
+    stage_exp(sv, tab_s);
     Grid g{};
     if constexpr (NQ == 0) g = stage_grid<SMEM>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     if (i >= n) return;
     double v[DIMF];
@@ -416,7 +452,11 @@ template <int KIND, int DIMF, bool SMEM>
 __global__ void vol_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
                                  const int64_t n, double* __restrict__ vols) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const Grid g = stage_grid<SMEM>(sv, smem);
+    __shared__ double2 tab_s[kExpTableSize];
+    stage_exp(sv, tab_s);
+    Grid g = stage_grid<SMEM>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double v[DIMF];
@@ -425,7 +465,7 @@ __global__ void vol_batch_kernel(const __grid_constant__ SurfaceView sv, const d
     const int nq = g.qoff[g.ns];
     const double omb = 1.0 - v[1];
     for (int s = 0; s < g.ns; ++s) {
-        const double pw = pow_fwd(omb, g.lnf_hi[s], g.lnf_lo[s]);
+        const double pw = pow_fwd(omb, g.lnf_hi[s], g.lnf_lo[s], g.tab);
         SmileTerms t;
         if constexpr (KIND == OBJ_STATIC) {
             t = static_terms(v[0], v[1], v[2], v[3], pw, g.T[s]);
