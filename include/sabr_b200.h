@@ -244,7 +244,12 @@ SABR_API sabr_status sabr_evaluate_case2_prices(sabr_ctx* ctx, const sabr_surfac
  *                   calibration.cpp:253-267 with :300-306
  *   CASE1  (dim 6): sum over slices, calibration.cpp:339-349 (slice must be -1)
  *   CASE2  (dim 11 incl. horizon): case2_mc_cost, calibration.cpp:399-416
- *                   (needs `plan`; infeasible vectors raise SABR_E_CONSTRAINT) */
+ *                   (needs `plan`; infeasible vectors raise SABR_E_CONSTRAINT)
+ *   SABR_OBJECTIVE_CASE2_FORMULA (dim 11): the calibrate_case2_formula
+ *                   objective, calibration.cpp:497-520 (dyn_coeffs_case2 with
+ *                   8-node Gauss-Legendre + Black-Scholes per quote; 1e10 when
+ *                   a formula vol leaves its validity range) */
+#define SABR_OBJECTIVE_CASE2_FORMULA 3
 SABR_API sabr_status sabr_cost_batch(sabr_ctx* ctx, int32_t model, const sabr_surface* surface,
                                      int64_t slice, const double* params, int64_t n,
                                      const sabr_plan* plan, double* cost);

@@ -350,6 +350,40 @@ SABR_API int ref_cost_case2_mc(const sabr_surface* s, const double* params, int6
     });
 }
 
+// The calibrate_case2_formula objective (calibration.cpp:497-520), restated
+// with the reference's own public functions; params n x 11 (horizon last).
+SABR_API int ref_cost_case2_formula(const sabr_surface* s, const double* params, int64_t n,
+                                    double* cost) {
+    return guarded([&] {
+        const auto surface = to_surface(s);
+        const auto market = market_prices(surface);
+        std::vector<double> forwards;
+        for (std::size_t i = 0; i < surface.slices.size(); ++i) forwards.push_back(surface.forward(i));
+        for (int64_t k = 0; k < n; ++k) {
+            const auto p = case2_params(params + 11 * k);
+            double sum = 0.0;
+            bool bad = false;
+            for (std::size_t i = 0; i < surface.slices.size() && !bad; ++i) {
+                const auto& sl = surface.slices[i];
+                const auto coeffs = dyn_coeffs_case2(p, sl.maturity, 8);
+                for (std::size_t j = 0; j < sl.quotes.size(); ++j) {
+                    const double vol = dynamic_implied_vol(coeffs, p.alpha, p.beta, sl.quotes[j].strike,
+                                                           forwards[i], sl.maturity);
+                    if (!(vol > 0)) {
+                        bad = true;
+                        break;
+                    }
+                    const double price = black_scholes_call(surface.spot, sl.quotes[j].strike, sl.rate,
+                                                            sl.dividend, sl.maturity, vol);
+                    const double rel = (market[i][j] - price) / market[i][j];
+                    sum += rel * rel;
+                }
+            }
+            cost[k] = bad ? 1e10 : sum;
+        }
+    });
+}
+
 SABR_API int ref_case2_feasible(const double* params, int64_t n, uint8_t* out) {
     return guarded([&] {
         for (int64_t k = 0; k < n; ++k) {

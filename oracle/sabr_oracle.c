@@ -314,6 +314,215 @@ double orc_cost_sensitivity(int model, const sabr_surface* s, int64_t slice, con
     return worst;
 }
 
+/* --------------------------------------------- Case II coefficients --- */
+
+/* GaussLegendreRule(n), quadrature.cpp:13-33 */
+static void gauss_legendre(int n, double* nodes, double* weights) {
+    const int m = (n + 1) / 2;
+    for (int i = 0; i < m; ++i) {
+        double x = cos(ORC_PI * (i + 0.75) / (n + 0.5));
+        double pp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int j = 2; j <= n; ++j) {
+                const double p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            pp = n * (x * p1 - p0) / (x * x - 1.0);
+            const double dx = p1 / pp;
+            x -= dx;
+            if (fabs(dx) < 1e-15) break;
+        }
+        nodes[i] = -x;
+        nodes[n - 1 - i] = x;
+        weights[i] = weights[n - 1 - i] = 2.0 / ((1.0 - x * x) * pp * pp);
+    }
+}
+
+/* detail::exp_moments, analytics.cpp:219-244 */
+static void exp_moments(double k, double T, double* out, int size) {
+    const double x = k * T;
+    if (x < 0.5) {
+        double tp = T;
+        for (int n = 0; n < size; ++n) {
+            double term = 1.0, sum = 1.0 / (n + 1);
+            for (int m = 1; m < 30; ++m) {
+                term *= -x / m;
+                const double contrib = term / (n + m + 1);
+                sum += contrib;
+                if (fabs(contrib) < 1e-18 * fabs(sum)) break;
+            }
+            out[n] = tp * sum;
+            tp *= T;
+        }
+        return;
+    }
+    const double e = exp(-x);
+    out[0] = (1.0 - e) / k;
+    double tp = 1.0;
+    for (int n = 1; n < size; ++n) {
+        tp *= T;
+        out[n] = (n * out[n - 1] - tp * e) / k;
+    }
+}
+
+/* integrate_poly_exp, analytics.cpp:80-86 */
+static double integrate_poly_exp(const double* p, int size, double k, double T) {
+    double mom[8] = {0};
+    exp_moments(k, T, mom, size);
+    double sum = 0.0;
+    for (int n = 0; n < size; ++n) sum += p[n] * mom[n];
+    return sum;
+}
+
+/* poly_mul, analytics.cpp:72-77; returns the product size */
+static int poly_mul(const double* p, int np, const double* q, int nq, double* r) {
+    for (int i = 0; i < np + nq - 1; ++i) r[i] = 0.0;
+    for (int i = 0; i < np; ++i)
+        for (int j = 0; j < nq; ++j) r[i + j] += p[i] * q[j];
+    return np + nq - 1;
+}
+
+typedef struct {
+    double k;
+    double poly[3];
+    int n;
+} piece_t;
+
+/* case2_nu_sq_pieces / case2_nurho_pieces, analytics.cpp:94-108 */
+static int nu_sq_pieces(const double* p, piece_t* out) {
+    const double nu_lin[2] = {p[5], p[6]};
+    out[0].k = 2 * p[9];
+    out[0].n = poly_mul(nu_lin, 2, nu_lin, 2, out[0].poly);
+    out[1].k = p[9];
+    out[1].poly[0] = 2 * p[7] * p[5];
+    out[1].poly[1] = 2 * p[7] * p[6];
+    out[1].n = 2;
+    out[2].k = 0.0;
+    out[2].poly[0] = p[7] * p[7];
+    out[2].n = 1;
+    return 3;
+}
+
+static int nurho_pieces(const double* p, piece_t* out) {
+    const double nu_lin[2] = {p[5], p[6]};
+    const double rho_lin[2] = {p[2], p[3]};
+    out[0].k = p[8] + p[9];
+    out[0].n = poly_mul(nu_lin, 2, rho_lin, 2, out[0].poly);
+    out[1].k = p[9];
+    out[1].poly[0] = p[4] * p[5];
+    out[1].poly[1] = p[4] * p[6];
+    out[1].n = 2;
+    out[2].k = p[8];
+    out[2].poly[0] = p[7] * p[2];
+    out[2].poly[1] = p[7] * p[3];
+    out[2].n = 2;
+    out[3].k = 0.0;
+    out[3].poly[0] = p[7] * p[4];
+    out[3].n = 1;
+    return 4;
+}
+
+/* integrate_pieces, analytics.cpp:110-116 */
+static double integrate_pieces(const piece_t* pieces, int np, const double* w, int nw, double T) {
+    double sum = 0.0;
+    for (int i = 0; i < np; ++i) {
+        double r[8];
+        const int n = poly_mul(w, nw, pieces[i].poly, pieces[i].n, r);
+        sum += integrate_poly_exp(r, n, pieces[i].k, T);
+    }
+    return sum;
+}
+
+/* detail::case2_inner_integral, analytics.cpp:246-251 */
+static double case2_inner_integral(const double* p, double s) {
+    piece_t pc[4];
+    const int np = nurho_pieces(p, pc);
+    double sum = 0.0;
+    for (int i = 0; i < np; ++i) sum += integrate_poly_exp(pc[i].poly, pc[i].n, pc[i].k, s);
+    return sum;
+}
+
+/* GaussLegendreRule::integrate, quadrature.hpp:18-25, for the two nested
+ * integrands of dyn_coeffs_case2 */
+typedef struct {
+    const double* p;
+    const double* x;
+    const double* w;
+    int n;
+    double layer;
+} gl_ctx;
+
+static double gl_inner(const gl_ctx* c, double lo, double hi) {
+    const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+    double sum = 0.0;
+    for (int i = 0; i < c->n; ++i) {
+        const double g = case2_inner_integral(c->p, mid + half * c->x[i]);
+        sum += c->w[i] * (g * g);
+    }
+    return half * sum;
+}
+
+static double integrate_inner(const gl_ctx* c, double hi) {
+    const double split = smin(c->layer, hi);
+    double sum = gl_inner(c, 0.0, split);
+    if (split < hi) sum += gl_inner(c, split, hi);
+    return sum;
+}
+
+static double gl_outer(const gl_ctx* c, double lo, double hi) {
+    const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+    double sum = 0.0;
+    for (int i = 0; i < c->n; ++i) sum += c->w[i] * integrate_inner(c, mid + half * c->x[i]);
+    return half * sum;
+}
+
+/* dyn_coeffs_case2, analytics.cpp:255-289 (p must be feasible: the caller
+ * validates, as the reference does on entry). */
+void orc_dyn_coeffs_case2(const double p[11], double T, int nodes, double out[4]) {
+    const double T2 = T * T, T3 = T2 * T, T4 = T3 * T;
+    piece_t nu_sq[3], nurho[4];
+    nu_sq_pieces(p, nu_sq);
+    nurho_pieces(p, nurho);
+    const double w1[3] = {T * T, -2.0 * T, 1.0};
+    const double w2[3] = {0.0, T, -1.0};
+    const double w3[2] = {T, -1.0};
+    out[0] = 3.0 / T3 * integrate_pieces(nu_sq, 3, w1, 3, T);
+    out[1] = 6.0 / T3 * integrate_pieces(nu_sq, 3, w2, 3, T);
+    out[2] = 2.0 / T2 * integrate_pieces(nurho, 4, w3, 2, T);
+    double x[64], w[64];
+    gauss_legendre(nodes, x, w);
+    const double rate = smax(p[8], p[9]);
+    gl_ctx c = {p, x, w, nodes, rate > 0 ? 10.0 / rate : T};
+    const double split = smin(c.layer, T);
+    double sum = gl_outer(&c, 0.0, split);
+    if (split < T) sum += gl_outer(&c, split, T);
+    out[3] = 12.0 / T4 * sum;
+}
+
+/* The calibrate_case2_formula objective, calibration.cpp:497-520 */
+double orc_cost_case2_formula(const sabr_surface* s, const double p[11]) {
+    double sum = 0.0;
+    for (int64_t i = 0; i < s->n_slices; ++i) {
+        const double T = s->maturity[i];
+        const double fwd = orc_forward(s, i);
+        double c[4];
+        orc_dyn_coeffs_case2(p, T, 8, c);
+        for (int64_t j = s->quote_offset[i]; j < s->quote_offset[i + 1]; ++j) {
+            const double vol = orc_dynamic_implied_vol(c, p[0], p[1], s->strike[j], fwd, T);
+            if (!(vol > 0)) return 1e10;
+            const double price = orc_black_scholes_call(s->spot, s->strike[j], s->rate[i],
+                                                        s->dividend[i], T, vol);
+            const double market = orc_black_scholes_call(s->spot, s->strike[j], s->rate[i],
+                                                         s->dividend[i], T, s->vol[j]);
+            const double rel = (market - price) / market;
+            sum += rel * rel;
+        }
+    }
+    return sum;
+}
+
 /* ------------------------------------------------------------ annealer --- */
 
 /* propose, annealer.cpp:60-74 (in place into `next`) */

@@ -47,6 +47,10 @@ int orc_case2_feasible(const double p[11]);
 /* Cost functions (proj/src/calibration.cpp:253-275, :300-306, :339-349) */
 double orc_cost_static(const sabr_surface* s, int64_t slice, const double p[4]);
 double orc_cost_case1(const sabr_surface* s, const double p[6]);
+/* dyn_coeffs_case2 (analytics.cpp:255-289, p feasible) and the
+ * calibrate_case2_formula objective (calibration.cpp:497-520) */
+void orc_dyn_coeffs_case2(const double p[11], double T, int nodes, double out[4]);
+double orc_cost_case2_formula(const sabr_surface* s, const double p[11]);
 /* |cost change| when exp/pow in the analytics move by one ulp (test bound). */
 double orc_cost_sensitivity(int model, const sabr_surface* s, int64_t slice, const double* p);
 

@@ -13,7 +13,10 @@
 
 #include "device_common.cuh"
 #include "engine.hpp"
+#include "kernels_c2f.hpp"
 #include "xoshiro_jump.hpp"
+
+#include <functional>
 
 // NCCL is loaded at run time (the one torch already mapped, else the system
 // library), so the engine has no link-time NCCL dependency.
@@ -177,10 +180,17 @@ struct T1Out {
 // minimize (annealer.cpp:76-167) for a device objective; `start_full` is the
 // full parameter vector (fixed entries at their values), only dims in
 // free_mask are searched.
-T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, uint32_t free_mask,
-                const std::vector<double>& lo, const std::vector<double>& hi,
-                const std::vector<double>& start_full, const sabr_schedule& sch, int builtin,
-                int pred) {
+using StartFn = std::function<cudaError_t(const SaLevelArgs&)>;
+using LevelFn = std::function<cudaError_t(const SaLevelArgs&, int64_t, double)>;
+
+// The device-resident level loop shared by every T_I-style objective:
+// `start` seeds incumbent/best values on the device, `level` launches one
+// temperature level (whose last CTA merges, or which writes the rank record
+// for the NCCL merge).  `records` = CTA records one level kernel writes.
+T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std::vector<double>& lo,
+                     const std::vector<double>& hi, const std::vector<double>& start_full,
+                     const sabr_schedule& sch, bool start_ok, int64_t records,
+                     const StartFn& start, const LevelFn& level_fn, int builtin, int pred) {
     validate_schedule(sch);
     // SearchSpace::validate, annealer.cpp:48-58
     if (free_mask == 0) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
@@ -191,7 +201,7 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
     for (int i = 0; i < dim_full; ++i)
         if (((free_mask >> i) & 1u) && (start_full[i] < lo[i] || start_full[i] > hi[i])) feasible = false;
     if (pred == SABR_PRED_SUM_LE_1 && !(start_full[0] + start_full[1] <= 1.0)) feasible = false;
-    if (!feasible) fail(SABR_E_DOMAIN, "annealer: start point is infeasible");
+    if (!feasible || !start_ok) fail(SABR_E_DOMAIN, "annealer: start point is infeasible");
 
     const std::vector<double> temps = temperatures(sch);
     const int64_t L = static_cast<int64_t>(temps.size());
@@ -205,8 +215,7 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
     st.done = (L == 0 || st.evals >= sch.max_evals) ? 1 : 0;
     st.eval_cap = st.done ? 0 : (sch.max_evals - st.evals + n_chains - 1) / n_chains;
 
-    const int threads = sa_block_threads();
-    const int64_t grid = std::max<int64_t>(1, (end - begin + threads - 1) / threads);
+    const int64_t grid = std::max<int64_t>(1, records);
     SaLevelArgs a{};
     for (int i = 0; i < dim_full; ++i) {
         a.lo[i] = lo[i];
@@ -236,7 +245,13 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
     a.trace_f = static_cast<double*>(dev_buf(ctx, "sa_trace", sizeof(double) * std::max<int64_t>(1, L)));
     check_cuda(cudaMemcpyAsync(a.state, &st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream), "H2D state");
     check_cuda(cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), ctx->stream), "memset ticket");
-    check_cuda(launch_sa_start(kind, sv, a, ctx->stream), "sa_start");
+    if (a.n_local == 0) {  // a rank without chains contributes an empty record every level
+        sabr_level_record empty{};
+        empty.end_chain = empty.best_chain = -1;
+        check_cuda(cudaMemcpyAsync(a.rank_rec, &empty, sizeof(empty), cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D record");
+    }
+    check_cuda(start(a), "sa_start");
 
     Timer timer(ctx);
     timer.start();
@@ -245,7 +260,7 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
     for (int64_t level = 0; level < L; ++level) {
         if (a.n_local > 0) {
             timer.before();
-            check_cuda(launch_sa_level(kind, sv, a, level, temps[level], ctx->stream), "sa_level");
+            check_cuda(level_fn(a, level, temps[level]), "sa_level");
             timer.after();
             ++launched;
         }
@@ -276,6 +291,93 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
     }
     r.trace_t.assign(temps.begin(), temps.begin() + out.levels_run);
     return r;
+}
+
+// minimize (annealer.cpp:76-167) for the thread-per-chain objectives.
+T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, uint32_t free_mask,
+                const std::vector<double>& lo, const std::vector<double>& hi,
+                const std::vector<double>& start_full, const sabr_schedule& sch, int builtin,
+                int pred) {
+    const int64_t n_chains = static_cast<int64_t>(sch.workers) * sch.groups;
+    const int64_t n_local = (ctx->rank + 1) * n_chains / ctx->nranks - ctx->rank * n_chains / ctx->nranks;
+    const int threads = sa_block_threads();
+    const int64_t records = (n_local + threads - 1) / threads;
+    cudaStream_t s = ctx->stream;
+    return run_sa_generic(
+        ctx, dim_full, free_mask, lo, hi, start_full, sch, true, records,
+        [&](const SaLevelArgs& a) { return launch_sa_start(kind, sv, a, s); },
+        [&](const SaLevelArgs& a, int64_t level, double temp) {
+            return launch_sa_level(kind, sv, a, level, temp, s);
+        },
+        builtin, pred);
+}
+
+// GaussLegendreRule(n), proj/src/quadrature.cpp:13-33 (same Newton iteration,
+// same nodes/weights to the last bit).
+void gauss_legendre(int n, double* nodes, double* weights) {
+    constexpr double kPi = 3.14159265358979323846;
+    const int m = (n + 1) / 2;
+    for (int i = 0; i < m; ++i) {
+        double x = std::cos(kPi * (i + 0.75) / (n + 0.5));
+        double pp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int j = 2; j <= n; ++j) {
+                const double p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            pp = n * (x * p1 - p0) / (x * x - 1.0);
+            const double dx = p1 / pp;
+            x -= dx;
+            if (std::abs(dx) < 1e-15) break;
+        }
+        nodes[i] = -x;
+        nodes[n - 1 - i] = x;
+        weights[i] = weights[n - 1 - i] = 2.0 / ((1.0 - x * x) * pp * pp);
+    }
+}
+
+// Device view of the calibrate_case2_formula objective (calibration.cpp:483-520).
+C2fView make_c2f_view(sabr_ctx* ctx, const HostSurface& s, const std::vector<double>& market,
+                      double horizon) {
+    if (s.n() > static_cast<size_t>(kMaxC2fSlices))
+        fail(SABR_E_DOMAIN, "calibrate_case2_formula: at most 64 slices on the device");
+    std::vector<C2fSlice> sl(s.n());
+    std::vector<C2fQuote> q(s.total_quotes());
+    for (size_t i = 0; i < s.n(); ++i) {
+        const double f = s.forward(i);
+        sl[i] = {s.T[i], std::sqrt(s.T[i]), f, s.r[i] - s.y[i]};
+        for (int64_t j = s.off[i]; j < s.off[i + 1]; ++j) {
+            const double lm = std::log(s.K[j] / f);
+            q[j] = {lm, lm * lm, std::log(s.spot / s.K[j]), s.spot * std::exp(-s.y[i] * s.T[i]),
+                    s.K[j] * std::exp(-s.r[i] * s.T[i]), market[j], 1.0 / market[j],
+                    static_cast<int32_t>(i), 0};
+        }
+    }
+    C2fView v{};
+    v.ns = static_cast<int32_t>(s.n());
+    v.nq = static_cast<int32_t>(s.total_quotes());
+    v.sl = upload(ctx, "c2f_slices", sl);
+    v.q = upload(ctx, "c2f_quotes", q);
+    v.horizon = horizon;
+    v.gl_n = 8;  // dyn_coeffs_case2(p, T, 8), calibration.cpp:506
+    gauss_legendre(v.gl_n, v.gl_x, v.gl_w);
+    v.exptab = exp_table_device(ctx);
+    return v;
+}
+
+std::vector<double> c2f_costs(sabr_ctx* ctx, const C2fView& v, const std::vector<double>& params11) {
+    const int64_t n = static_cast<int64_t>(params11.size()) / 11;
+    std::vector<double> out(n);
+    if (n == 0) return out;
+    double* dp = upload(ctx, "c2f_params", params11);
+    double* dc = static_cast<double*>(dev_buf(ctx, "c2f_cost", sizeof(double) * n));
+    check_cuda(launch_c2f_cost(v, dp, n, dc, ctx->stream), "c2f_cost");
+    check_cuda(cudaMemcpyAsync(out.data(), dc, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream),
+               "D2H cost");
+    sync(ctx);
+    return out;
 }
 
 // Objective value(s) of full vectors on the device.
@@ -676,7 +778,13 @@ void validate_model(int model, const double* p) {
     fail(SABR_E_DOMAIN, "unknown model");
 }
 
+// Paths per thread: a function of the plan alone (it fixes the payoff
+// reduction tree, so prices never depend on the batch or the GPU count).
+// Large plans amortise the xoshiro jump over 4 consecutive paths; plans
+// below 2^18 paths keep one path per thread so even a single candidate fills
+// the 148 SMs.
 int choose_ppt(const sabr_plan& plan) {
+    if (plan.num_paths < (1ull << 18)) return 1;
     if (plan.rng == SABR_RNG_PHILOX) return 4;
     for (int p : {4, 2})
         if (plan.block_size % p == 0) return p;
@@ -1074,12 +1182,76 @@ SABR_API sabr_status sabr_calibrate_case2_T2(sabr_ctx* ctx, const sabr_surface* 
     });
 }
 
-SABR_API sabr_status sabr_calibrate_case2_formula(sabr_ctx* ctx, const sabr_surface*,
-                                                  const sabr_bounds*, const sabr_schedule*,
-                                                  const sabr_fixed*, sabr_report*) {
+// calibrate_case2_formula, proj/src/calibration.cpp:483-534
+SABR_API sabr_status sabr_calibrate_case2_formula(sabr_ctx* ctx, const sabr_surface* surface_in,
+                                                  const sabr_bounds* bounds,
+                                                  const sabr_schedule* schedule,
+                                                  const sabr_fixed* fixed, sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
-        fail(SABR_E_LOGIC, "calibrate_case2_formula: not available in this build");
+        if (!schedule) fail(SABR_E_INVALID, "schedule is null");
+        const HostSurface surface = HostSurface::from_abi(surface_in);
+        surface.validate();
+        const auto t0 = std::chrono::steady_clock::now();
+        const double horizon = surface.T.back();
+        const ParamSpace ps(case2_defs(), bounds_from_abi(bounds), fixed_from_abi(fixed),
+                            atm_vol_guess(surface, 0));
+        const auto market = market_prices(surface);
+        const C2fView v = make_c2f_view(ctx, surface, market, horizon);
+        auto with_h = [&](std::vector<double> x) {
+            x.push_back(horizon);
+            return x;
+        };
+        Report rep{"case2", "T_I", "price"};
+        std::vector<double> best_full;
+        if (ps.free_ix.empty()) {  // run_or_evaluate: one objective call (dyn_coeffs_case2 validates)
+            best_full = ps.full({});
+            validate_case2(with_h(best_full).data());
+            double c = c2f_costs(ctx, v, with_h(best_full))[0];
+            rep.final_cost = c;
+            rep.evals = 1;
+        } else {
+            validate_schedule(*schedule);
+            const auto start = ps.full(ps.start_point());
+            const bool start_ok = case2_feasible_host(with_h(start).data());
+            double v0 = 0.0;
+            if (start_ok) {
+                v0 = c2f_costs(ctx, v, with_h(start))[0];
+                if (std::isnan(v0)) v0 = INFINITY;  // safe_eval, annealer.cpp:84-87
+            }
+            std::vector<double> lo(10), hi(10);
+            for (int i = 0; i < 10; ++i) {
+                lo[i] = ps.defs[i].lo;
+                hi[i] = ps.defs[i].hi;
+            }
+            const int64_t n_chains = static_cast<int64_t>(schedule->workers) * schedule->groups;
+            const int64_t n_local =
+                (ctx->rank + 1) * n_chains / ctx->nranks - ctx->rank * n_chains / ctx->nranks;
+            cudaStream_t s = ctx->stream;
+            const T1Out r = run_sa_generic(
+                ctx, 10, ps.free_mask(), lo, hi, start, *schedule, start_ok, n_local,
+                [&](const SaLevelArgs& a) {
+                    cudaError_t e = cudaMemcpyAsync(&a.state->incumbent_value, &v0, sizeof(double),
+                                                    cudaMemcpyHostToDevice, s);
+                    if (e != cudaSuccess) return e;
+                    e = cudaMemcpyAsync(&a.state->best_value, &v0, sizeof(double), cudaMemcpyHostToDevice, s);
+                    if (e != cudaSuccess) return e;
+                    return cudaStreamSynchronize(s);  // v0 lives on this stack frame
+                },
+                [&](const SaLevelArgs& a, int64_t level, double temp) {
+                    return launch_c2f_level(v, a, level, temp, s);
+                },
+                0, SABR_PRED_NONE);
+            best_full = r.best_full;
+            rep.final_cost = r.best_value;
+            rep.evals = r.evals;
+            rep.trace_t = r.trace_t;
+            rep.trace_f = r.trace_f;
+        }
+        rep.params = ps.named(best_full);
+        rep.seed = schedule->seed;
+        rep.wall_seconds = seconds_since(t0);
+        rep.write(report);
     });
 }
 
@@ -1125,6 +1297,14 @@ SABR_API sabr_status sabr_cost_batch(sabr_ctx* ctx, int32_t model, const sabr_su
             for (int64_t i = 0; i < n; ++i) validate_case1(params + 6 * i);
             const SurfaceView sv = make_view(ctx, "view_case1", surface, nullptr);
             const auto c = device_costs(ctx, OBJ_CASE1, sv, std::vector<double>(params, params + 6 * n), 6);
+            std::copy(c.begin(), c.end(), cost);
+        } else if (model == SABR_OBJECTIVE_CASE2_FORMULA) {
+            if (slice != -1) fail(SABR_E_DOMAIN, "case2 objective is joint: slice must be -1");
+            surface.validate();
+            const auto market = market_prices(surface);
+            for (int64_t i = 0; i < n; ++i) validate_case2(params + 11 * i);  // dyn_coeffs_case2 validates
+            const C2fView v = make_c2f_view(ctx, surface, market, surface.T.back());
+            const auto c = c2f_costs(ctx, v, std::vector<double>(params, params + 11 * n));
             std::copy(c.begin(), c.end(), cost);
         } else if (model == SABR_MODEL_CASE2) {
             if (!plan) fail(SABR_E_INVALID, "case2 objective needs a plan");

@@ -399,3 +399,26 @@ def cost_sensitivity(orc, model, surface, slice, params):
     return np.array([orc.lib.orc_cost_sensitivity(C.c_int(model), C.byref(s), C.c_int64(slice),
                                                   _dptr(np.ascontiguousarray(P[i])))
                      for i in range(P.shape[0])])
+
+
+def ref_cost_case2_formula(ref, surface, params):
+    s, keep = surface.to_abi()
+    P = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 11)
+    out = np.empty(P.shape[0])
+    ref._check(ref.lib.ref_cost_case2_formula(C.byref(s), _dptr(P), C.c_int64(P.shape[0]), _dptr(out)))
+    return out
+
+
+def orc_cost_case2_formula(orc, surface, params):
+    orc.lib.orc_cost_case2_formula.restype = C.c_double
+    s, keep = surface.to_abi()
+    P = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 11)
+    return np.array([orc.lib.orc_cost_case2_formula(C.byref(s), _dptr(np.ascontiguousarray(P[i])))
+                     for i in range(P.shape[0])])
+
+
+def orc_dyn_coeffs_case2(orc, p, T, nodes=8):
+    v = np.ascontiguousarray(p, dtype=np.float64)
+    out = np.zeros(4)
+    orc.lib.orc_dyn_coeffs_case2(_dptr(v), C.c_double(T), C.c_int(nodes), _dptr(out))
+    return out

@@ -101,3 +101,15 @@ def test_case2_T2_matches_reference(engine, ref, eq_surface):
         assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
     for a, b in zip(g.rows, r.rows):
         assert abs(a.model - b.model) <= 1e-9 * abs(b.model)
+
+
+def test_case2_formula_matches_reference(engine, ref, fx_surface):
+    """calibrate_case2_formula (calibration.cpp:483-534) end to end."""
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=8, workers=16, t_min=0.05, seed=2)
+    g = engine.calibrate_case2_formula(fx_surface, None, s, {"beta": 1.0})
+    r = ref.calibrate_case2_formula(fx_surface, None, s, {"beta": 1.0})
+    assert g.model == "case2" and g.technique == "T_I" and g.quantity == "price" and not g.rows
+    assert g.evals == r.evals
+    assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
+    for k in r.params:
+        assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k

@@ -127,3 +127,38 @@ def test_domain_errors(engine, eq_surface):
         engine.cost_batch(pkg.MODEL_CASE1, eq_surface, np.array([[0.3, 1.0, -0.5, 0.0, 0.1, 0.1]]))
     with pytest.raises(pkg.OutOfRangeError):
         engine.cost_batch(pkg.MODEL_STATIC, eq_surface, np.array([[0.3, 1.0, 0.5, 0.0]]), slice=9)
+
+
+def feasible_case2_vectors(ref, n, seed, horizon):
+    rng = np.random.default_rng(seed)
+    lo = np.array([1e-4, 0, -1, -15, -1, 1e-4, -15, -1, 0, 0])
+    hi = np.array([2, 1, 1, 15, 1, 10, 15, 1, 150, 150])
+    out = []
+    while len(out) < n:
+        P = lo + (hi - lo) * rng.random((4 * n, 10))
+        P[:, 3] *= rng.random(4 * n) ** 3  # favour the feasible region
+        P[:, 6] *= rng.random(4 * n) ** 3
+        P = np.column_stack([P, np.full(len(P), horizon)])
+        out.extend(P[ref.case2_feasible(P)])
+    return np.array(out[:n])
+
+
+@pytest.mark.parametrize("fixture", ["eq_surface", "fx_surface"])
+def test_case2_formula_cost_parity(engine, ref, request, fixture):
+    """calibrate_case2_formula objective (calibration.cpp:497-520): nested GL
+    eta2^2 + Black-Scholes, CTA-cooperative on the GPU vs the reference."""
+    from oracles import ref_cost_case2_formula
+
+    surface = request.getfixturevalue(fixture)
+    H = surface.slices[-1].maturity
+    P = feasible_case2_vectors(ref, 300, 5, H)
+    pub = np.array([[0.296790, 1.0, -0.360610, 15.0, -0.715716, 0.000100, -8.969205, 0.847244, 15.0, 15.0, H],
+                    [0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807, 0.0, 150.0, H]])
+    P = np.vstack([pub[ref.case2_feasible(pub)], P])
+    got = engine.cost_batch(3, surface, P)
+    want = ref_cost_case2_formula(ref, surface, P)
+    assert np.array_equal(got == 1e10, want == 1e10)  # same "left its validity range" verdicts
+    ok = want != 1e10
+    rel = np.abs(got[ok] - want[ok]) / np.maximum(np.abs(want[ok]), 1e-8)
+    print(f"case2 formula {fixture}: {ok.sum()} finite, max rel {rel.max():.2e}")
+    assert rel.max() < 1e-10

@@ -1,0 +1,50 @@
+"""Refresh profiles/fp64_per_eval.json from a round's ncu metric CSVs
+(gpurun_out/ncu_metrics_{sa,case1,t2,mc}.csv) and copy them to profiles/<tag>_*."""
+import json
+import os
+import shutil
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_summary import summarise  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def per(path, prefix, units, pick=-1):
+    mets = [m for k, m in summarise(path).items() if k.startswith(prefix)]
+    m = mets[pick]
+    g = {k: sum(v) / len(v) for k, v in m.items()}
+    dfma = g["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"]
+    dadd = g["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
+    dmul = g["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"]
+    return ((2 * dfma + dadd + dmul) / units, (dfma + dadd + dmul) / units,
+            g["dram__bytes_read.sum"] + g["dram__bytes_write.sum"], g["gpu__time_duration.sum"])
+
+
+def main(tag):
+    src = os.path.join(ROOT, "gpurun_out")
+    sa = per(os.path.join(src, "ncu_metrics_sa.csv"), "sa_level_kernel<0", 1e7)
+    c1 = per(os.path.join(src, "ncu_metrics_case1.csv"), "sa_level_kernel<1", 1e7)
+    t2 = per(os.path.join(src, "ncu_metrics_t2.csv"), "mc_tile_kernel<8", 32 * 1e5 * 250)
+    mc = per(os.path.join(src, "ncu_metrics_mc.csv"), "mc_tile_kernel<1", (1 << 20) * 124)
+    d = {"source": f"ncu smsp__sass_thread_inst_executed_op_{{dfma,dadd,dmul}}_pred_on.sum (DFMA = 2 FLOP) "
+                   f"per unit, profiles/{tag}_ncu_metrics_*.csv (tools/profile_kernels.py)",
+         "c2_flops_per_eval": sa[0], "c2_fp64_instr_per_eval": sa[1], "c2_dram_bytes_per_launch": sa[2],
+         "c2_level_kernel_ns": sa[3],
+         "c3_flops_per_eval": c1[0], "c3_fp64_instr_per_eval": c1[1], "c3_dram_bytes_per_launch": c1[2],
+         "c3_level_kernel_ns": c1[3],
+         "c4_flops_per_candidate_path_step": t2[0], "c4_fp64_instr_per_candidate_path_step": t2[1],
+         "c4_dram_bytes_per_launch": t2[2], "c4_mc_kernel_ns": t2[3],
+         "mc_single_flops_per_path_step": mc[0], "mc_single_fp64_instr_per_path_step": mc[1]}
+    with open(os.path.join(ROOT, "profiles", "fp64_per_eval.json"), "w") as f:
+        json.dump(d, f, indent=1)
+    for m in ("sa", "case1", "t2", "t2_cb4", "mc"):
+        p = os.path.join(src, f"ncu_metrics_{m}.csv")
+        if os.path.exists(p):
+            shutil.copy(p, os.path.join(ROOT, "profiles", f"{tag}_ncu_metrics_{m}.csv"))
+    print(json.dumps(d, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
