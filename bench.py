@@ -278,26 +278,30 @@ def secondary(eng, torch, dev, stream):
     import paper_2407_20713_b200 as pkg
 
     out = {}
-    surf, fixed, sch, plan = c4_setup(levels=2)
-    small = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=32, t_min=1.5, seed=1)
-    eng.calibrate_case2_T2(surf, None, small, plan, fixed)  # warm-up (jump tables, buffers)
-    flush_l2(torch, dev)
-    torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    rep = eng.calibrate_case2_T2(surf, None, sch, plan, fixed)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    t = eng.last_timing()
-    secs = e0.elapsed_time(e1) / 1e3
-    steps_per_eval = 250
-    ps = (rep.evals - 1) * plan.num_paths * steps_per_eval
-    out["c4_mc_calibration"] = {
-        "metric": "MC SABR path-steps/s (calibrate_case2_T2 objective, C4)", "unit": "path-steps/s",
-        "value": ps / secs, "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
-        "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,
-        "steps_per_path": steps_per_eval, "rng": plan.rng, "seconds": secs,
-        "mc_kernel_ms": t.kernel_ms, "mc_launches": t.kernel_launches}
+    for precision in ("fp64", "fp32"):
+        surf, fixed, sch, plan = c4_setup(levels=2)
+        plan.precision = precision
+        small = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=32, t_min=1.5, seed=1)
+        eng.calibrate_case2_T2(surf, None, small, plan, fixed)  # warm-up (jump tables, buffers)
+        flush_l2(torch, dev)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        rep = eng.calibrate_case2_T2(surf, None, sch, plan, fixed)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = eng.last_timing()
+        secs = e0.elapsed_time(e1) / 1e3
+        steps_per_eval = 250
+        ps = (rep.evals - 1) * plan.num_paths * steps_per_eval
+        key = "c4_mc_calibration" if precision == "fp64" else "c4_mc_calibration_fp32"
+        out[key] = {
+            "metric": f"MC SABR path-steps/s (calibrate_case2_T2 objective, C4, {precision})",
+            "unit": "path-steps/s", "value": ps / secs,
+            "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
+            "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,
+            "steps_per_path": steps_per_eval, "rng": plan.rng, "precision": precision, "seconds": secs,
+            "final_cost": rep.final_cost, "mc_kernel_ms": t.kernel_ms, "mc_launches": t.kernel_launches}
     # C3: Case I joint calibration, EUR/USD, beta = 1 (acceptance.cpp:317-339 schedule, 1e5 chains)
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
     s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8, t_min=1e-7,

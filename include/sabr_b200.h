@@ -85,6 +85,13 @@ typedef struct sabr_schedule {
     uint64_t seed;
 } sabr_schedule;
 
+/* Arithmetic of the Monte Carlo path loop.  FP64 is the reference's
+ * precision and the parity path.  FP32 is the opt-in fast path: the same
+ * streams and the same log-Euler scheme with FP32 state and MUFU exp2 per
+ * candidate-step (normals from FP32 library functions, payoff sums in FP64);
+ * prices agree with FP64 on identical streams to ~1e-5 relative. */
+typedef enum sabr_precision { SABR_FP64 = 0, SABR_FP32 = 1 } sabr_precision;
+
 /* SimulationPlan (proj/include/sabr/mc.hpp:12-20) plus the stream choice. */
 typedef struct sabr_plan {
     uint64_t num_paths;
@@ -93,6 +100,8 @@ typedef struct sabr_plan {
     int32_t workers; /* accepted, validated, ignored */
     int32_t rng;     /* sabr_rng */
     uint64_t block_size;
+    int32_t precision; /* sabr_precision */
+    int32_t _pad;
 } sabr_plan;
 
 /* BoundsOverrides / FixedParams (calibration.hpp:77-79). */

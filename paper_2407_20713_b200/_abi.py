@@ -23,6 +23,7 @@ STATUS_NAMES = {
 
 MODEL_STATIC, MODEL_CASE1, MODEL_CASE2 = 0, 1, 2
 RNG_XOSHIRO, RNG_PHILOX = 0, 1
+FP64, FP32 = 0, 1
 
 OBJ_BOWL3, OBJ_ROSENBROCK4, OBJ_SINQUAD2, OBJ_SQUARE1, OBJ_COSBOWL2, OBJ_CORNER2, OBJ_NANRIGHT1 = range(7)
 PRED_NONE, PRED_SUM_LE_1 = 0, 1
@@ -70,6 +71,8 @@ class sabr_plan(C.Structure):
         ("workers", C.c_int32),
         ("rng", C.c_int32),
         ("block_size", C.c_uint64),
+        ("precision", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 

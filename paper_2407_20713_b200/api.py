@@ -196,7 +196,9 @@ class AnnealingSchedule:
 @dataclass
 class SimulationPlan:
     """SimulationPlan, mc.hpp:12-20, plus the random stream (``"xoshiro"``
-    reproduces the reference streams; ``"philox"`` is counter-based)."""
+    reproduces the reference streams; ``"philox"`` is counter-based) and the
+    path-loop arithmetic (``"fp64"``, the reference's; ``"fp32"``, the MUFU
+    fast path)."""
 
     num_paths: int = 1 << 20
     dt: float = 1.0 / 250.0
@@ -204,10 +206,12 @@ class SimulationPlan:
     workers: int = 1
     block_size: int = 4096
     rng: str = "xoshiro"
+    precision: str = "fp64"
 
     def to_abi(self) -> A.sabr_plan:
         rng = {"xoshiro": A.RNG_XOSHIRO, "philox": A.RNG_PHILOX}[self.rng]
-        return A.sabr_plan(self.num_paths, self.dt, self.seed, self.workers, rng, self.block_size)
+        prec = {"fp64": A.FP64, "fp32": A.FP32}[self.precision]
+        return A.sabr_plan(self.num_paths, self.dt, self.seed, self.workers, rng, self.block_size, prec, 0)
 
     def validate(self) -> None:
         """SimulationPlan::validate, mc.cpp:161-166."""

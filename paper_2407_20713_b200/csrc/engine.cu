@@ -581,6 +581,21 @@ void check_cuda(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(SABR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Host-built per-step coefficients (one candidate) for the chosen path-loop
+// arithmetic: FP64 rows, plus their FP32 copy for SABR_FP32.
+void set_coefficients(sabr_ctx* ctx, McParams& P, const std::vector<StepCoef>& coef, int precision) {
+    P.coef = upload(ctx, "mc_coef", coef);
+    P.fp32 = precision == SABR_FP32 ? 1 : 0;
+    P.coef32 = nullptr;
+    if (P.fp32) {
+        std::vector<float4> c32(coef.size());
+        for (size_t i = 0; i < coef.size(); ++i)
+            c32[i] = make_float4(static_cast<float>(coef[i].c1), static_cast<float>(coef[i].c2),
+                                 static_cast<float>(coef[i].rs), static_cast<float>(coef[i].ss));
+        P.coef32 = upload(ctx, "mc_coef32", c32);
+    }
+}
+
 const double2* exp_table_device(sabr_ctx* ctx) {
     auto it = ctx->bufs.find("exptab");
     if (it != ctx->bufs.end()) return static_cast<const double2*>(it->second.first);
@@ -872,7 +887,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.alpha0 = upload(ctx, "mc_alpha0", std::vector<double>{alpha0});
     P.beta = upload(ctx, "mc_beta", std::vector<double>{beta});
     P.active = nullptr;
-    P.coef = upload(ctx, "mc_coef", coef);
+    set_coefficients(ctx, P, coef, plan.precision);
     P.cand_stride = 1;
     P.hdt = upload(ctx, "mc_hdt", job.hdt);
     P.strikes = upload(ctx, "mc_strikes", strikes);
@@ -1415,7 +1430,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
         P.slices = upload(ctx, "mc_slices", job.slices);
         P.alpha0 = upload(ctx, "mc_alpha0", std::vector<double>{alpha0});
         P.beta = upload(ctx, "mc_beta", std::vector<double>{params[1]});
-        P.coef = upload(ctx, "mc_coef", coef);
+        set_coefficients(ctx, P, coef, plan->precision);
         P.cand_stride = 1;
         P.hdt = upload(ctx, "mc_hdt", job.hdt);
         P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});

@@ -126,6 +126,8 @@ inline void validate_plan(const sabr_plan& p) {
     if (p.block_size < 1) fail(SABR_E_DOMAIN, "SimulationPlan: block_size must be >= 1");
     if (p.rng != SABR_RNG_XOSHIRO && p.rng != SABR_RNG_PHILOX)
         fail(SABR_E_DOMAIN, "SimulationPlan: unknown rng");
+    if (p.precision != SABR_FP64 && p.precision != SABR_FP32)
+        fail(SABR_E_DOMAIN, "SimulationPlan: unknown precision");
     if (p.num_paths > (1ull << 40)) fail(SABR_E_DOMAIN, "SimulationPlan: num_paths too large");
 }
 

@@ -107,7 +107,8 @@ cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2
 // per (candidate, step) coefficients of build_grid (mc.cpp:69-82) on device
 cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
                            int32_t cand_stride, const double* t_end, const double* dt,
-                           const double* sdt, int64_t total_steps, void* coef, cudaStream_t s);
+                           const double* sdt, int64_t total_steps, void* coef, int fp32,
+                           cudaStream_t s);
 // Metropolis (annealer.cpp:123-134) with the MC costs of this step
 cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double* cost,
                              const int* bad, int* nonfinite, cudaStream_t s);

@@ -189,6 +189,163 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     }
 }
 
+// The FP32 fast path: the same streams (uniforms drawn in FP64 exactly as the
+// reference draws them), the same log-Euler step carried in FP32 state with
+// one MUFU ex2 per candidate-step; normals from accurate FP32 library
+// functions; F_T = F0 exp(x) and the payoff sums in FP64.
+template <int CB>
+__global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid_constant__ McParams P) {
+    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
+
+    int64_t idx = blockIdx.x;
+    const int tile = static_cast<int>(idx % P.n_tiles);
+    idx /= P.n_tiles;
+    const int s = static_cast<int>(idx % P.n_slices);
+    const int g = static_cast<int>(idx / P.n_slices);
+    const McSlice sl = P.slices[s];
+    const int c0 = g * CB;
+    const int mq = sl.q_end - sl.q_begin;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    uint32_t act_mask = 0, logn_mask = 0;
+    float la0[CB], bm1[CB];
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+        const int c = c0 + cc;
+        const bool act = c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
+        act_mask |= act ? (1u << cc) : 0u;
+        la0[cc] = act ? static_cast<float>(log(P.alpha0[c])) : 0.0f;
+        bm1[cc] = act ? static_cast<float>(P.beta[c] - 1.0) : 0.0f;
+        logn_mask |= (act && P.beta[c] == 1.0) || !act ? (1u << cc) : 0u;
+    }
+    if (act_mask == 0) return;  // block-uniform
+
+    const bool reduce = P.partials != nullptr;
+    if (reduce) {
+        for (int i = threadIdx.x; i < kWarps * CB * mq * 2; i += kMcThreads) acc[i] = 0.0;
+        __syncthreads();
+    }
+
+    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
+    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+
+    Xoshiro rng;
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t k = (p0 % P.block_size) / P.ppt;
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
+
+    const int64_t cstride = P.cand_stride;
+    const float4* __restrict__ crow0 = P.coef32 + static_cast<int64_t>(sl.step_off) * cstride + c0;
+    const double* __restrict__ hdt = P.hdt + sl.step_off;
+    const float lnf0 = static_cast<float>(sl.lnf0);
+
+    for (int k = 0; k < P.ppt; ++k) {
+        const uint64_t path = p0 + k;
+        const bool live = path < P.num_paths;
+        float la[CB], x[CB];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            la[cc] = la0[cc];
+            x[cc] = 0.0f;
+        }
+        if (live) {
+            auto normals = [&](int i, float& z1, float& z2) {
+                double ua, ub;
+                if (P.rng == SABR_RNG_XOSHIRO) {
+                    ua = rng.uniform();
+                    ub = rng.uniform();
+                } else {
+                    philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
+                }
+                // box_muller, mc.cpp:30-36: u1 = 1 - U in (0,1] (exact in FP64)
+                const float r = sqrtf(-2.0f * logf(static_cast<float>(1.0 - ua)));
+                float sn, cs;
+                sincospif(static_cast<float>(2.0 * ub), &sn, &cs);
+                z1 = r * cs;
+                z2 = r * sn;
+            };
+            auto advance_all = [&](float h, const float4* q, float z1, float z2) {
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) {
+                    const float arg = ((logn_mask >> cc) & 1u) ? la[cc] : fmaf(bm1[cc], lnf0 + x[cc], la[cc]);
+                    const float nh = __expf(arg);  // MUFU.EX2
+                    la[cc] += fmaf(q[cc].x, z1, -q[cc].y);
+                    const float u = fmaf(q[cc].w, z2, q[cc].z * z1);
+                    x[cc] = fmaf(nh, fmaf(-nh, h, u), x[cc]);
+                }
+            };
+            // step i+1's coefficients are loaded while step i computes (the
+            // L1 latency of these uniform loads was the top stall)
+            float4 q[CB], qn[CB];
+            const float4* crow = crow0;
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) qn[cc] = __ldg(crow + cc);
+            float hn = static_cast<float>(__ldg(hdt));
+            float z1, z2;
+            normals(0, z1, z2);
+            const int n = sl.n_steps;
+            for (int i = 0; i + 1 < n; ++i) {
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) q[cc] = qn[cc];
+                const float h = hn;
+                crow += cstride;
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) qn[cc] = __ldg(crow + cc);
+                hn = static_cast<float>(__ldg(hdt + i + 1));
+                float n1, n2;
+                normals(i + 1, n1, n2);
+                advance_all(h, q, z1, z2);
+                z1 = n1;
+                z2 = n2;
+            }
+            advance_all(hn, qn, z1, z2);
+        }
+        double F[CB];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            F[cc] = sl.forward0 * exp(static_cast<double>(x[cc]));
+            if (live && ((act_mask >> cc) & 1u) && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);
+        }
+        if (P.terminals != nullptr && live) P.terminals[path] = F[0];
+        if (!reduce) continue;
+        for (int j = 0; j < mq; ++j) {
+            const double K = __ldg(P.strikes + sl.q_begin + j);
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) {
+                if (!((act_mask >> cc) & 1u)) continue;
+                const double d = F[cc] - K;
+                const double v = live ? sl.discount * ((d < 0.0) ? 0.0 : d) : 0.0;
+                const double s1 = warp_sum(v);
+                const double s2 = warp_sum(v * v);
+                if (lane == 0) {
+                    double* slot = acc + ((warp * CB + cc) * mq + j) * 2;
+                    slot[0] += s1;
+                    slot[1] += s2;
+                }
+            }
+        }
+    }
+    if (!reduce) return;
+    __syncthreads();
+    for (int t = threadIdx.x; t < CB * mq; t += kMcThreads) {
+        const int cc = t / mq, j = t % mq;
+        if (c0 + cc >= P.n_cand) continue;
+        double s1 = 0.0, s2 = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            s1 += acc[((w * CB + cc) * mq + j) * 2];
+            s2 += acc[((w * CB + cc) * mq + j) * 2 + 1];
+        }
+        double* out = P.partials +
+                      ((static_cast<int64_t>(c0 + cc) * P.n_quotes + sl.q_begin + j) * P.n_tiles + tile) * 2;
+        out[0] = s1;
+        out[1] = s2;
+    }
+}
+
 // reduce_payoffs (mc.cpp:146-157) over the tiles, in tile order.
 __global__ void mc_reduce_kernel(const McParams P, double* __restrict__ value,
                                  double* __restrict__ std_error) {
@@ -228,7 +385,7 @@ template <int CB>
 cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     const int mq = p.max_q;
     const size_t smem = p.partials ? static_cast<size_t>(kWarps) * CB * mq * 2 * sizeof(double) : 0;
-    auto k = mc_tile_kernel<CB>;
+    auto k = p.fp32 ? mc_tile_kernel_f32<CB> : mc_tile_kernel<CB>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -249,6 +406,7 @@ cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s) {
         case 2: return tiles_t<2>(p, s);
         case 4: return tiles_t<4>(p, s);
         case 8: return tiles_t<8>(p, s);
+        case 16: return tiles_t<16>(p, s);
     }
     return cudaErrorInvalidValue;
 }

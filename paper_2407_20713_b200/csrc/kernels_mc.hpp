@@ -52,6 +52,8 @@ struct McParams {
     double* terminals;      // [num_paths] (n_cand == 1, n_slices == 1) or null
     int* bad;               // [n_cand] non-finite flag
     const double2* exptab;  // [128] 2^(i/128) double-double (exp_tab, device_common.cuh)
+    int32_t fp32;           // SABR_FP32: the FP32/MUFU path loop (coef32 instead of coef)
+    const float4* coef32;   // [total_steps][cand_stride] {c1, c2, rs, ss} in FP32
 };
 
 // The exp_tab table, built once on the host in long double.

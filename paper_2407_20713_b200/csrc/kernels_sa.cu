@@ -571,13 +571,14 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t
                                const int32_t n_local, const int32_t cand_stride,
                                const double* __restrict__ t_end, const double* __restrict__ dt,
                                const double* __restrict__ sdt, const int64_t total_steps,
-                               double4* __restrict__ coef) {
+                               double4* __restrict__ coef, float4* __restrict__ coef32) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<int64_t>(cand_stride) * total_steps) return;
     const int c = static_cast<int>(t % cand_stride);
     const int64_t i = t / cand_stride;
     if (c >= n_local || !active[c]) {
-        coef[t] = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (coef32) coef32[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        else coef[t] = make_double4(0.0, 0.0, 0.0, 0.0);
         return;
     }
     const T2Chain& ch = chains[c];
@@ -589,7 +590,10 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t
     const double q = 1.0 - rho * rho;
     const double srho = sqrt((0.0 < q) ? q : 0.0);
     const double s = sdt[i];
-    coef[t] = make_double4(nu * s, 0.5 * nu * nu * dt[i], rho * s, srho * s);
+    const double4 v = make_double4(nu * s, 0.5 * nu * nu * dt[i], rho * s, srho * s);
+    if (coef32) coef32[t] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
+                                        static_cast<float>(v.z), static_cast<float>(v.w));
+    else coef[t] = v;
 }
 
 __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
@@ -854,11 +858,13 @@ cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2
 
 cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
                            int32_t cand_stride, const double* t_end, const double* dt,
-                           const double* sdt, int64_t total_steps, void* coef, cudaStream_t s) {
+                           const double* sdt, int64_t total_steps, void* coef, int fp32,
+                           cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(cand_stride) * total_steps;
     if (n <= 0) return cudaSuccess;
     t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        chains, active, n_local, cand_stride, t_end, dt, sdt, total_steps, static_cast<double4*>(coef));
+        chains, active, n_local, cand_stride, t_end, dt, sdt, total_steps,
+        fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr);
     return cudaGetLastError();
 }
 

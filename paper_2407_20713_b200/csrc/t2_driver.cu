@@ -73,10 +73,13 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     const int64_t per_cand = S * 32 + static_cast<int64_t>(nq) * n_tiles * 16;
     const int32_t chunk = static_cast<int32_t>(
         std::max<int64_t>(1, std::min<int64_t>(std::max(n_local, 1), (int64_t(1) << 31) / std::max<int64_t>(per_cand, 1))));
+    const bool fp32 = plan.precision == SABR_FP32;
+    // candidates per thread: 8 (register bound in FP64; in FP32 the
+    // coefficient prefetch buffer takes the room a 16-wide group would need)
     int cb = chunk >= 8 ? 8 : (chunk >= 4 ? 4 : (chunk >= 2 ? 2 : 1));
-    if (const char* e = std::getenv("SABR_MC_CB")) {  // tuning override (1, 2, 4, 8)
+    if (const char* e = std::getenv("SABR_MC_CB")) {  // tuning override (1, 2, 4, 8, 16)
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || v == 8) cb = std::min(v, cb);
+        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) cb = std::min(v, cb);
     }
     const int32_t stride = (chunk + cb - 1) / cb * cb;  // coefficient row width
 
@@ -108,7 +111,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     auto* cost = static_cast<double*>(dev_buf(ctx, "t2_cost", sizeof(double) * nl));
     auto* bad = static_cast<int*>(dev_buf(ctx, "t2_bad", sizeof(int) * nl));
     auto* nonfinite = static_cast<int*>(dev_buf(ctx, "t2_nonfinite", sizeof(int)));
-    auto* coef = static_cast<StepCoef*>(dev_buf(ctx, "t2_coef", sizeof(StepCoef) * S * stride));
+    void* coef = dev_buf(ctx, "t2_coef", (fp32 ? sizeof(float4) : sizeof(StepCoef)) * S * stride);
     auto* partials = static_cast<double*>(
         dev_buf(ctx, "t2_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * n_tiles * chunk));
     auto* values = static_cast<double*>(dev_buf(ctx, "t2_values", sizeof(double) * static_cast<size_t>(nq) * chunk));
@@ -168,13 +171,15 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
                 const int32_t nc = std::min(chunk, n_local - c0);
                 const int32_t nc_pad = (nc + cb - 1) / cb * cb;
                 check_cuda(launch_t2_coef(chains + c0, active + c0, nc, nc_pad, d_tend, d_dt, d_sdt, S,
-                                          coef, ctx->stream), "t2_coef");
+                                          coef, fp32 ? 1 : 0, ctx->stream), "t2_coef");
                 McParams Q = P;
                 Q.n_cand = nc;
                 Q.alpha0 = alpha0 + c0;
                 Q.beta = beta + c0;
                 Q.active = active + c0;
-                Q.coef = coef;
+                Q.fp32 = fp32 ? 1 : 0;
+                Q.coef = fp32 ? nullptr : static_cast<const StepCoef*>(coef);
+                Q.coef32 = fp32 ? static_cast<const float4*>(coef) : nullptr;
                 Q.cand_stride = nc_pad;
                 Q.partials = partials;
                 Q.terminals = nullptr;

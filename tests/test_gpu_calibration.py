@@ -103,6 +103,21 @@ def test_case2_T2_matches_reference(engine, ref, eq_surface):
         assert abs(a.model - b.model) <= 1e-9 * abs(b.model)
 
 
+def test_case2_T2_fp32_fast_path(engine, eq_surface):
+    """The FP32 MC objective drives the same annealer: the same proposals are
+    evaluated (evals depend on feasibility only) and the calibrated cost stays
+    within the FP32 price tolerance of the FP64 run's neighbourhood."""
+    surf = pkg.VolSurface(eq_surface.spot, [eq_surface.slices[2]])
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=4, workers=32, t_min=0.2, seed=3)
+    p64 = pkg.SimulationPlan(num_paths=1 << 14, seed=1)
+    p32 = pkg.SimulationPlan(num_paths=1 << 14, seed=1, precision="fp32")
+    a = engine.calibrate_case2_T2(surf, None, s, p64, fixed)
+    b = engine.calibrate_case2_T2(surf, None, s, p32, fixed)
+    assert a.evals == b.evals
+    assert abs(a.final_cost - b.final_cost) <= 1e-2 * a.final_cost
+
+
 def test_case2_formula_matches_reference(engine, ref, fx_surface):
     """calibrate_case2_formula (calibration.cpp:483-534) end to end."""
     s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=8, workers=16, t_min=0.05, seed=2)

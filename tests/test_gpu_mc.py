@@ -120,3 +120,37 @@ def test_published_fx_prices_case2(engine, fx_surface):
         for j in range(3):
             worst = max(worst, abs(est[j].value - want[i][j]) / est[j].std_error)
     assert worst < 3.0, worst
+
+
+@pytest.mark.parametrize("params", [K_STATIC, K_CASE1, K_CASE2, pkg.StaticSabrParams(0.3, 0.7, 0.5, -0.4)])
+@pytest.mark.parametrize("rng", ["xoshiro", "philox"])
+def test_fp32_fast_path_tracks_fp64_on_identical_streams(engine, params, rng):
+    """SABR_FP32: same streams, FP32 state + MUFU ex2.  Stated tolerance:
+    per-path F_T within 1e-5 relative, prices within 2e-5 relative of FP64
+    (the paper's FP32/FP64 price gap is 6e-6)."""
+    p64 = plan(n=1 << 16, seed=9, rng=rng)
+    p32 = plan(n=1 << 16, seed=9, rng=rng)
+    p32.precision = "fp32"
+    a = engine.simulate_terminals(params, F0, params.alpha, T, p64)
+    b = engine.simulate_terminals(params, F0, params.alpha, T, p32)
+    assert np.max(np.abs(a - b) / a) < 1e-5
+    strikes = [0.9 * F0, F0, 1.1 * F0]
+    x = engine.price_european_batch(params, F0, strikes, 0.018196, 0.034516, T, p64)
+    y = engine.price_european_batch(params, F0, strikes, 0.018196, 0.034516, T, p32)
+    for u, v in zip(x, y):
+        assert abs(u.value - v.value) <= 2e-5 * u.value
+
+
+def test_fp32_published_fx_prices(engine, fx_surface):
+    # acceptance c8 with the FP32 path: still within 3 sigma of the published prices
+    p = pkg.CaseIIParams(0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807,
+                         0.0, 150.0, 2.0)
+    want = [[0.101712, 0.040476, 0.011697], [0.144950, 0.056139, 0.015539],
+            [0.198897, 0.075409, 0.020010], [0.260539, 0.101766, 0.028189]]
+    pl = plan(n=1 << 20, seed=5)
+    pl.precision = "fp32"
+    for i, s in enumerate(fx_surface.slices):
+        strikes = [s.quotes[c].strike for c in (3, 9, 15)]
+        est = engine.price_european_batch(p, fx_surface.spot, strikes, s.rate, s.dividend, s.maturity, pl)
+        for j in range(3):
+            assert abs(est[j].value - want[i][j]) < 3.0 * est[j].std_error

@@ -30,7 +30,8 @@ def main(mode):
         surf = pkg.VolSurface(eq.spot, [eq.slices[2]])
         fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
         s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=3, workers=32, t_min=1.5, seed=1)
-        plan = pkg.SimulationPlan(num_paths=100_000, seed=1, rng=os.environ.get("SABR_RNG", "xoshiro"))
+        plan = pkg.SimulationPlan(num_paths=100_000, seed=1, rng=os.environ.get("SABR_RNG", "xoshiro"),
+                                  precision=os.environ.get("SABR_PRECISION", "fp64"))
         r = eng.calibrate_case2_T2(surf, None, s, plan, fixed)
     elif mode == "mc":
         plan = pkg.SimulationPlan(num_paths=1 << 20, seed=3, rng=os.environ.get("SABR_RNG", "xoshiro"))
