@@ -923,6 +923,114 @@ int orc_simulate_terminals(int model, const double* params, double forward0, dou
     return bad ? SABR_E_RUNTIME : SABR_OK;
 }
 
+/* run_path with observation nodes, mc.cpp:87-107 (obs recorded after step
+ * i+1 == node; node 0 is never recorded) */
+static void run_path_obs(const grid_t* g, double forward0, double alpha0, int rng_mode,
+                         orc_xoshiro* xo, uint64_t seed, uint64_t path, const int* nodes, int n_obs,
+                         double* out) {
+    double alpha = alpha0, forward = forward0;
+    int next = 0;
+    for (int i = 0; i < g->n; ++i) {
+        double ua, ub;
+        if (rng_mode == SABR_RNG_XOSHIRO) {
+            ua = orc_xoshiro_uniform(xo);
+            ub = orc_xoshiro_uniform(xo);
+        } else {
+            orc_philox_uniform_pair(seed, path, (uint32_t)i, &ua, &ub);
+        }
+        double z1, z2;
+        box_muller(ua, ub, &z1, &z2);
+        const double nu = g->nu[i], dt = g->dt[i], sdt = g->sqrt_dt[i];
+        const double alpha_next = alpha * exp(nu * z1 * sdt - 0.5 * nu * nu * dt);
+        const double nu_hat = g->lognormal ? alpha : alpha * pow(forward, g->beta - 1.0);
+        forward *= exp(nu_hat * (g->rho[i] * z1 + g->srho[i] * z2) * sdt - 0.5 * nu_hat * nu_hat * dt);
+        alpha = alpha_next;
+        if (next < n_obs && nodes[next] == i + 1) out[next++] = forward;
+    }
+}
+
+/* price_cliquet, mc.cpp:275-320 */
+int orc_price_cliquet(int model, const double* params, double spot, double rate, double dividend,
+                      double lf, double lc, double gf, double gc, const double* resets, int n_resets,
+                      const sabr_plan* plan, double* value, double* se) {
+    if (lf > lc || gf > gc || n_resets < 2) return SABR_E_DOMAIN;
+    for (int i = 0; i < n_resets; ++i)
+        if (resets[i] <= 0 || (i > 0 && resets[i] <= resets[i - 1])) return SABR_E_DOMAIN;
+    if (!plan_valid(plan) || !(spot > 0)) return SABR_E_DOMAIN;
+    int st = model_status(model, params);
+    if (st != SABR_OK) return st;
+    const double maturity = resets[n_resets - 1];
+    const double forward0 = spot * exp((rate - dividend) * maturity);
+    grid_t g;
+    st = build_grid(model, params, maturity, plan->dt, &g);
+    if (st != SABR_OK) return st;
+    double* node_time = malloc(sizeof(double) * (g.n + 1));
+    node_time[0] = 0.0;
+    double acc = 0.0;
+    for (int i = 0; i < g.n; ++i) {  /* node_time of build_grid, mc.cpp:59-68 */
+        const int extra = (i == g.n - 1) && g.dt[i] != plan->dt;
+        acc = extra ? maturity : smin((double)(i + 1) * plan->dt, maturity);
+        node_time[i + 1] = acc;
+    }
+    int nodes[256];
+    double disc[256];
+    for (int k = 0; k < n_resets; ++k) {
+        int best = 0;
+        for (int j = 1; j <= g.n; ++j)
+            if (fabs(node_time[j] - resets[k]) < fabs(node_time[best] - resets[k])) best = j;
+        if (fabs(node_time[best] - resets[k]) > 0.5 * plan->dt + 1e-12 ||
+            (k > 0 && best <= nodes[k - 1])) {
+            free(node_time);
+            grid_free(&g);
+            return SABR_E_DOMAIN;
+        }
+        nodes[k] = best;
+        disc[k] = exp(-(rate - dividend) * (maturity - node_time[best]));
+    }
+    const size_t n = plan->num_paths;
+    double* rows = calloc(n * (size_t)n_resets, sizeof(double));
+    int bad = 0;
+    if (plan->rng == SABR_RNG_XOSHIRO) {
+        const uint64_t n_blocks = (n + plan->block_size - 1) / plan->block_size;
+        for (uint64_t b = 0; b < n_blocks; ++b) {
+            orc_xoshiro rng;
+            orc_xoshiro_init(&rng, plan->seed, b);
+            const uint64_t begin = b * plan->block_size;
+            const uint64_t end = begin + plan->block_size < n ? begin + plan->block_size : n;
+            for (uint64_t p = begin; p < end; ++p)
+                run_path_obs(&g, forward0, params[0], SABR_RNG_XOSHIRO, &rng, 0, 0, nodes, n_resets,
+                             rows + p * n_resets);
+        }
+    } else {
+        for (uint64_t p = 0; p < n; ++p)
+            run_path_obs(&g, forward0, params[0], SABR_RNG_PHILOX, NULL, plan->seed, p, nodes, n_resets,
+                         rows + p * n_resets);
+    }
+    for (size_t i = 0; i < n * (size_t)n_resets; ++i)
+        if (!isfinite(rows[i])) bad = 1;
+    const double discount = exp(-rate * maturity);
+    double sum = 0.0, sum_sq = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double* row = rows + i * n_resets;
+        double s = 0.0;
+        for (int j = 1; j < n_resets; ++j) {
+            const double s_prev = row[j - 1] * disc[j - 1];
+            const double s_cur = row[j] * disc[j];
+            s += sclamp((s_cur - s_prev) / s_prev, lf, lc);
+        }
+        const double v = discount * sclamp(s, gf, gc);
+        sum += v;
+        sum_sq += v * v;
+    }
+    const double mean = sum / (double)n;
+    *value = mean;
+    *se = sqrt(smax(0.0, (sum_sq - (double)n * mean * mean) / ((double)n - 1.0)) / (double)n);
+    free(rows);
+    free(node_time);
+    grid_free(&g);
+    return bad ? SABR_E_RUNTIME : SABR_OK;
+}
+
 /* price_european_batch + reduce_payoffs, mc.cpp:146-157, :249-273 */
 int orc_price_european_batch(int model, const double* params, double spot,
                              const double* strikes, int64_t m, double rate, double dividend,

@@ -86,6 +86,10 @@ int orc_price_european_batch(int model, const double* params, double spot,
                              double T, const sabr_plan* plan, double* value, double* se);
 double orc_black_scholes_call(double spot, double strike, double r, double y, double T,
                               double vol);
+/* price_cliquet, mc.cpp:275-320 */
+int orc_price_cliquet(int model, const double* params, double spot, double rate, double dividend,
+                      double lf, double lc, double gf, double gc, const double* resets, int n_resets,
+                      const sabr_plan* plan, double* value, double* se);
 /* case2_mc_cost (calibration.cpp:399-416); params 11 (horizon last). */
 int orc_cost_case2_mc(const sabr_surface* s, const double p[11], const sabr_plan* plan,
                       double* cost);

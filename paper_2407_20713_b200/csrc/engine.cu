@@ -1476,12 +1476,115 @@ SABR_API sabr_status sabr_mc_price_european_batch(sabr_ctx* ctx, int32_t model, 
     });
 }
 
-SABR_API sabr_status sabr_mc_price_cliquet(sabr_ctx* ctx, int32_t, const double*, double, double,
-                                           double, double, double, double, double, const double*,
-                                           int64_t, const sabr_plan*, double*, double*) {
+// mc::price_cliquet, proj/src/mc.cpp:275-320
+SABR_API sabr_status sabr_mc_price_cliquet(sabr_ctx* ctx, int32_t model, const double* params,
+                                           double spot, double rate, double dividend,
+                                           double local_floor, double local_cap, double global_floor,
+                                           double global_cap, const double* reset_dates,
+                                           int64_t n_resets, const sabr_plan* plan, double* value,
+                                           double* std_error) {
     return guarded([&] {
         CtxLock l(ctx);
-        fail(SABR_E_LOGIC, "price_cliquet: not available in this build");
+        if (!plan || !value || !std_error || (n_resets > 0 && !reset_dates))
+            fail(SABR_E_INVALID, "null argument");
+        validate_model(model, params);
+        // CliquetSpec::validate, mc.cpp:168-181
+        if (local_floor > local_cap) fail(SABR_E_DOMAIN, "CliquetSpec: local floor above local cap");
+        if (global_floor > global_cap) fail(SABR_E_DOMAIN, "CliquetSpec: global floor above global cap");
+        if (n_resets < 2) fail(SABR_E_DOMAIN, "CliquetSpec: need at least two reset dates");
+        for (int64_t i = 0; i < n_resets; ++i) {
+            if (reset_dates[i] <= 0) fail(SABR_E_DOMAIN, "CliquetSpec: reset dates must be positive");
+            if (i > 0 && reset_dates[i] <= reset_dates[i - 1])
+                fail(SABR_E_DOMAIN, "CliquetSpec: reset dates must be strictly increasing");
+        }
+        validate_plan(*plan);
+        if (spot <= 0) fail(SABR_E_DOMAIN, "price_cliquet: spot must be positive");
+        if (n_resets > kMaxCliquetObs) fail(SABR_E_DOMAIN, "price_cliquet: at most 128 reset dates");
+        const double maturity = reset_dates[n_resets - 1];
+        const double forward0 = spot * std::exp((rate - dividend) * maturity);
+        const HostGrid g = build_grid(maturity, plan->dt);
+        // snap each reset date to the nearest grid node (mc.cpp:285-300)
+        std::vector<double> node_time{0.0};
+        node_time.insert(node_time.end(), g.t_end.begin(), g.t_end.end());
+        CliquetSpecDev spec{};
+        spec.n_obs = static_cast<int32_t>(n_resets);
+        spec.local_floor = local_floor;
+        spec.local_cap = local_cap;
+        spec.global_floor = global_floor;
+        spec.global_cap = global_cap;
+        for (int64_t k = 0; k < n_resets; ++k) {
+            const double d = reset_dates[k];
+            size_t best = 0;
+            for (size_t j = 1; j < node_time.size(); ++j)
+                if (std::abs(node_time[j] - d) < std::abs(node_time[best] - d)) best = j;
+            if (std::abs(node_time[best] - d) > 0.5 * plan->dt + 1e-12)
+                fail(SABR_E_DOMAIN, "price_cliquet: reset date not within dt/2 of a grid node");
+            if (k > 0 && static_cast<int32_t>(best) <= spec.obs_node[k - 1])
+                fail(SABR_E_DOMAIN, "price_cliquet: reset dates collapse onto one grid node");
+            spec.obs_node[k] = static_cast<int32_t>(best);
+            spec.obs_discount[k] = std::exp(-(rate - dividend) * (maturity - node_time[best]));
+        }
+        const double alpha0 = params[0];
+        if (forward0 <= 0 || alpha0 < 0)
+            fail(SABR_E_DOMAIN, "mc: forward0 must be positive and alpha0 nonnegative");
+        const int ppt = choose_ppt(*plan);
+        McJob job;
+        job.slices.resize(1);
+        const auto jump = mc_layout(ctx, *plan, ppt, {g}, job);
+        std::vector<StepCoef> coef;
+        for (size_t i = 0; i < g.dt.size(); ++i) {
+            const double nu = model_nu_at(model, params, g.t_end[i]);
+            const double rho = model_rho_at(model, params, g.t_end[i]);
+            const double srho = std::sqrt(std::max(0.0, 1.0 - rho * rho));
+            coef.push_back({nu * g.sdt[i], 0.5 * nu * nu * g.dt[i], rho * g.sdt[i], srho * g.sdt[i]});
+        }
+        McSlice& sl = job.slices[0];
+        sl.q_begin = 0;
+        sl.q_end = 1;
+        sl.forward0 = forward0;
+        sl.lnf0 = std::log(forward0);
+        sl.discount = std::exp(-rate * maturity);
+        McParams P{};
+        P.n_slices = 1;
+        P.n_cand = 1;
+        P.n_quotes = 1;
+        P.max_q = 1;
+        P.ppt = ppt;
+        P.n_tiles = static_cast<int32_t>((plan->num_paths + static_cast<uint64_t>(kMcThreads) * ppt - 1) /
+                                         (static_cast<uint64_t>(kMcThreads) * ppt));
+        P.rng = plan->rng;
+        P.total_steps = job.total_steps;
+        P.num_paths = plan->num_paths;
+        P.block_size = plan->block_size;
+        P.seed = plan->seed;
+        P.slices = upload(ctx, "mc_slices", job.slices);
+        P.alpha0 = upload(ctx, "mc_alpha0", std::vector<double>{alpha0});
+        P.beta = upload(ctx, "mc_beta", std::vector<double>{params[1]});
+        set_coefficients(ctx, P, coef, SABR_FP64);
+        P.cand_stride = 1;
+        P.hdt = upload(ctx, "mc_hdt", job.hdt);
+        P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});
+        P.jump = upload(ctx, "mc_jump", jump);
+        P.exptab = exp_table_device(ctx);
+        P.partials = static_cast<double*>(dev_buf(ctx, "mc_partials", sizeof(double) * 2 * P.n_tiles));
+        P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
+        check_cuda(cudaMemsetAsync(P.bad, 0, sizeof(int), ctx->stream), "memset bad");
+        double* dv = static_cast<double*>(dev_buf(ctx, "mc_value", sizeof(double)));
+        double* ds = static_cast<double*>(dev_buf(ctx, "mc_se", sizeof(double)));
+        Timer timer(ctx);
+        timer.start();
+        timer.before();
+        check_cuda(launch_mc_cliquet(P, spec, ctx->stream), "mc_cliquet");
+        timer.after();
+        check_cuda(launch_mc_reduce(P, dv, ds, nullptr, nullptr, ctx->stream), "mc_reduce");
+        int bad = 0;
+        check_cuda(cudaMemcpyAsync(value, dv, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check_cuda(cudaMemcpyAsync(std_error, ds, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check_cuda(cudaMemcpyAsync(&bad, P.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        sync(ctx);
+        timer.stop(static_cast<double>(plan->num_paths) * job.total_steps,
+                   static_cast<double>(plan->num_paths) * job.total_steps, 1, 2);
+        if (bad) fail(SABR_E_RUNTIME, "mc: non-finite path value (scheme unstable for these inputs)");
     });
 }
 

@@ -346,6 +346,101 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
     }
 }
 
+// price_cliquet (mc.cpp:275-320): the path is observed at the reset nodes
+// (run_path records F after step i+1 == node, mc.cpp:104-105) and the payoff
+// sum_j clamp((S_j - S_{j-1}) / S_{j-1}, local) -> clamp(., global) is
+// accumulated on the fly (mc.cpp:308-318); discounted payoffs reduced as in
+// the European tile kernel (one partial per tile).
+__global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_constant__ McParams P,
+                                                                 const __grid_constant__ CliquetSpecDev C) {
+    __shared__ double acc[kWarps][2];
+    __shared__ double2 tab[kExpTableSize];
+    for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
+    if (threadIdx.x < kWarps * 2) (&acc[0][0])[threadIdx.x] = 0.0;
+    __syncthreads();
+    const int tile = blockIdx.x;
+    const McSlice sl = P.slices[0];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool logn = P.beta[0] == 1.0;
+    const double bm1 = P.beta[0] - 1.0;
+    const double la0 = log(P.alpha0[0]);
+    const uint64_t p0 = static_cast<uint64_t>(tile) * kMcThreads * P.ppt + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+    Xoshiro rng;
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>((p0 % P.block_size) / P.ppt));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
+    // an observation at node 0 is never recorded by run_path: the reference
+    // then observes nothing at all (mc.cpp:104), all observations stay 0
+    const bool none = C.n_obs > 0 && C.obs_node[0] == 0;
+    for (int k = 0; k < P.ppt; ++k) {
+        const uint64_t path = p0 + k;
+        const bool live = path < P.num_paths;
+        double v = 0.0;
+        if (live) {
+            double la = la0, x = 0.0, s_prev = 0.0, strip = 0.0;
+            bool finite = true;
+            int next = 0;
+            if (none) {
+                // all rows 0: ret = (0 - 0) / 0 for every pair
+                for (int j = 1; j < C.n_obs; ++j) {
+                    const double ret = (0.0 - 0.0) / 0.0;
+                    strip += (ret < C.local_floor) ? C.local_floor : (C.local_cap < ret) ? C.local_cap : ret;
+                }
+                next = C.n_obs;  // still draw the whole path: later paths continue the stream
+            }
+            for (int i = 0; i < sl.n_steps; ++i) {
+                double ua, ub;
+                if (P.rng == SABR_RNG_XOSHIRO) {
+                    ua = rng.uniform();
+                    ub = rng.uniform();
+                } else {
+                    philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
+                }
+                double z1, z2;
+                box_muller(ua, ub, z1, z2);
+                const StepCoef q = P.coef[sl.step_off + i];
+                const double nh = exp_tab(logn ? la : fma(bm1, sl.lnf0 + x, la), tab);
+                la += fma(q.c1, z1, -q.c2);
+                const double u = fma(q.ss, z2, q.rs * z1);
+                x = fma(nh, fma(-nh, __ldg(P.hdt + sl.step_off + i), u), x);
+                if (next < C.n_obs && C.obs_node[next] == i + 1) {
+                    const double F = sl.forward0 * exp_tab(x, tab);
+                    finite = finite && isfinite(F);
+                    const double s_cur = F * C.obs_discount[next];
+                    if (next > 0) {
+                        const double ret = (s_cur - s_prev) / s_prev;
+                        strip += (ret < C.local_floor) ? C.local_floor : (C.local_cap < ret) ? C.local_cap : ret;
+                    }
+                    s_prev = s_cur;
+                    ++next;
+                }
+            }
+            if (!finite) atomicOr(P.bad, 1);  // mc.cpp:133-138
+            const double g = (strip < C.global_floor) ? C.global_floor : (C.global_cap < strip) ? C.global_cap : strip;
+            v = sl.discount * g;
+        }
+        const double s1 = warp_sum(v);
+        const double s2 = warp_sum(v * v);
+        if (lane == 0) {
+            acc[warp][0] += s1;
+            acc[warp][1] += s2;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int w = 0; w < kWarps; ++w) {
+            s1 += acc[w][0];
+            s2 += acc[w][1];
+        }
+        P.partials[static_cast<int64_t>(tile) * 2] = s1;
+        P.partials[static_cast<int64_t>(tile) * 2 + 1] = s2;
+    }
+}
+
 // reduce_payoffs (mc.cpp:146-157) over the tiles, in tile order.
 __global__ void mc_reduce_kernel(const McParams P, double* __restrict__ value,
                                  double* __restrict__ std_error) {
@@ -409,6 +504,12 @@ cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s) {
         case 16: return tiles_t<16>(p, s);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mc_cliquet(const McParams& p, const CliquetSpecDev& spec, cudaStream_t s) {
+    if (p.n_tiles <= 0) return cudaSuccess;
+    mc_cliquet_kernel<<<static_cast<unsigned>(p.n_tiles), kMcThreads, 0, s>>>(p, spec);
+    return cudaGetLastError();
 }
 
 // {RN(2^(i/128)), RN(2^(i/128) - hi)} from x86 long double (64-bit mantissa):

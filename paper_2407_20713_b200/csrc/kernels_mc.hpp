@@ -59,6 +59,20 @@ struct McParams {
 // The exp_tab table, built once on the host in long double.
 const double2* exp_table_host();
 
+// price_cliquet (mc.cpp:275-320): observation nodes (step counts) and their
+// F -> S factors exp(-(r-y)(T - t_node)).
+constexpr int kMaxCliquetObs = 128;
+struct CliquetSpecDev {
+    int32_t n_obs;
+    int32_t obs_node[kMaxCliquetObs];
+    double obs_discount[kMaxCliquetObs];
+    double local_floor, local_cap, global_floor, global_cap;
+};
+
+// One candidate, one slice (McParams with n_cand = n_slices = 1, no strikes):
+// per-path clamped return strip, tile partials of (sum, sum of squares).
+cudaError_t launch_mc_cliquet(const McParams& p, const CliquetSpecDev& spec, cudaStream_t s);
+
 constexpr int kMcThreads = 128;
 
 // Simulate + fused payoff reduction per tile (price_european_batch,

@@ -121,6 +121,25 @@ def main():
                            "terminals_sum": hx(float(np.sum(t))),
                            "prices": [[hx(e.value), hx(e.std_error)] for e in est]}
 
+    # price_cliquet (mc.cpp:275-320), the acceptance c9 spec
+    K_FX1 = pkg.CaseIParams(0.155464, 0.971908, -0.642617, 0.800275, 0.001, 2.6093)
+    out["cliquet"] = {}
+    for name, dt in (("dt250", 1 / 250), ("dt007", 0.07)):
+        plan = pkg.SimulationPlan(num_paths=3000, seed=3, block_size=1000, dt=dt)
+        e = ref.price_cliquet(K_FX1, 1.2939, 0.010832, 0.006907, -0.02, 0.02, 0.0, 0.2, [0.25, 0.5, 0.75, 1.0],
+                              plan)
+        out["cliquet"][name] = {"dt": dt, "value": hx(e.value), "std_error": hx(e.std_error)}
+
+    # Case II coefficient functionals and the calibrate_case2_formula objective
+    P2 = np.array([[0.296790, 1.0, -0.360610, 15.0, -0.715716, 0.000100, -8.969205, 0.847244, 15.0, 15.0, 2.0],
+                   [0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807, 0.0, 150.0,
+                    2.0]])
+    from oracles import ref_cost_case2_formula
+    out["case2_formula"] = {"params": hx(P2),
+                            "coeffs": [[hx(ref.dyn_coeffs_case2(p, T, 8)) for T in (0.25, 1.0, 2.0)] for p in P2],
+                            "eurusd": hx(ref_cost_case2_formula(ref, fx, P2)),
+                            "eurostoxx50": hx(ref_cost_case2_formula(ref, eq, P2))}
+
     # calibrate_* reports
     s = pkg.AnnealingSchedule(t0=1.0, cooling=0.8, chain_length=10, workers=4, t_min=1e-2, seed=1)
     rep = ref.calibrate_static_T1(fx, 0, {"nu": (0.01, 3.0)}, s, {"beta": 0.75, "rho": -0.4})

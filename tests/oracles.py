@@ -422,3 +422,16 @@ def orc_dyn_coeffs_case2(orc, p, T, nodes=8):
     out = np.zeros(4)
     orc.lib.orc_dyn_coeffs_case2(_dptr(v), C.c_double(T), C.c_int(nodes), _dptr(out))
     return out
+
+
+def orc_price_cliquet(orc, params, spot, r, y, lf, lc, gf, gc, resets, plan):
+    model, v = model_of(params)
+    v = np.asarray(v, dtype=np.float64)
+    R = np.asarray(resets, dtype=np.float64)
+    val, se = C.c_double(), C.c_double()
+    pl = plan.to_abi()
+    st = orc.lib.orc_price_cliquet(C.c_int(model), _dptr(v), *(C.c_double(x) for x in (spot, r, y, lf, lc, gf, gc)),
+                                   _dptr(R), C.c_int(len(R)), C.byref(pl), C.byref(val), C.byref(se))
+    if st != 0:
+        raise_for_status(st, "oracle restatement: status %d" % st)
+    return PriceEstimate(val.value, se.value, int(plan.num_paths))

@@ -141,6 +141,45 @@ def test_fp32_fast_path_tracks_fp64_on_identical_streams(engine, params, rng):
         assert abs(u.value - v.value) <= 2e-5 * u.value
 
 
+def test_degenerate_cliquet_is_deterministic(engine):
+    # test_mc.cpp:116-128: local floor == local cap pins every return
+    p = pkg.StaticSabrParams(0.3, 1.0, 0.5, -0.3)
+    r, y = 0.010832, 0.006907
+    est = engine.price_cliquet(p, 1.2939, r, y, 0.02, 0.02, 0.0, 0.2, [0.25, 0.5, 0.75, 1.0],
+                               plan(n=1 << 12, seed=8))
+    want = np.exp(-r * 1.0) * min(max(3 * 0.02, 0.0), 0.2)
+    assert abs(est.value - want) <= 1e-14 * want
+    assert est.std_error == 0.0
+
+
+def test_cliquet_validation_errors(engine):
+    # test_mc.cpp:130-144
+    p = pkg.StaticSabrParams(0.3, 1.0, 0.5, -0.3)
+    pl = plan(n=16, seed=9)
+    with pytest.raises(pkg.DomainError):
+        engine.price_cliquet(p, 100.0, 0.0, 0.0, 0.02, -0.02, 0.0, 0.2, [0.5, 1.0], pl)
+    with pytest.raises(pkg.DomainError):
+        engine.price_cliquet(p, 100.0, 0.0, 0.0, -0.02, 0.02, 0.0, 0.2, [0.5, 0.5], pl)
+    with pytest.raises(pkg.DomainError, match="collapse"):
+        engine.price_cliquet(p, 100.0, 0.0, 0.0, -0.02, 0.02, 0.0, 0.2, [0.0005, 0.001, 1.0], pl)
+
+
+@pytest.mark.parametrize("which", ["case1", "case2"])
+def test_cliquet_matches_reference_streams(engine, ref, which):
+    """acceptance c9 payload (acceptance.cpp:288-315) on identical xoshiro streams."""
+    if which == "case1":
+        p = pkg.CaseIParams(0.155464, 0.971908, -0.642617, 0.800275, 0.001, 2.6093)
+    else:
+        p = pkg.CaseIIParams(0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551,
+                             0.339807, 0.0, 150.0, 2.0)
+    pl = plan(n=1 << 16, seed=3)
+    args = (1.2939, 0.010832, 0.006907, -0.02, 0.02, 0.0, 0.2, [0.25, 0.5, 0.75, 1.0], pl)
+    g = engine.price_cliquet(p, *args)
+    r = ref.price_cliquet(p, *args)
+    assert abs(g.value - r.value) <= 1e-10 * abs(r.value)
+    assert abs(g.std_error - r.std_error) <= 1e-8 * r.std_error
+
+
 def test_fp32_published_fx_prices(engine, fx_surface):
     # acceptance c8 with the FP32 path: still within 3 sigma of the published prices
     p = pkg.CaseIIParams(0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807,

@@ -171,3 +171,26 @@ class TestAgainstLiveReference:
         plan = pkg.SimulationPlan(num_paths=512, seed=1)
         a, b = orc.cost_case2_mc(fxs, P, plan), ref.cost_case2_mc(fxs, P, plan)
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["dt250", "dt007"])
+def test_cliquet_golden(orc, name):
+    from oracles import orc_price_cliquet
+
+    g = GOLDEN["cliquet"][name]
+    p = pkg.CaseIParams(0.155464, 0.971908, -0.642617, 0.800275, 0.001, 2.6093)
+    plan = pkg.SimulationPlan(num_paths=3000, seed=3, block_size=1000, dt=g["dt"])
+    e = orc_price_cliquet(orc, p, 1.2939, 0.010832, 0.006907, -0.02, 0.02, 0.0, 0.2, [0.25, 0.5, 0.75, 1.0], plan)
+    assert e.value == fx(g["value"]) and e.std_error == fx(g["std_error"])
+
+
+def test_case2_formula_golden(orc):
+    from oracles import orc_cost_case2_formula, orc_dyn_coeffs_case2
+
+    g = GOLDEN["case2_formula"]
+    P = fx(g["params"])
+    for p, coeffs in zip(P, g["coeffs"]):
+        for T, c in zip((0.25, 1.0, 2.0), coeffs):
+            assert np.array_equal(orc_dyn_coeffs_case2(orc, p, T, 8), fx(c))
+    for name in ("eurusd", "eurostoxx50"):
+        assert np.array_equal(orc_cost_case2_formula(orc, golden_surface(name), P), fx(g[name]))
