@@ -28,6 +28,25 @@ SABR_HD uint64_t splitmix64(uint64_t& state) {
 
 SABR_HD uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
 
+// 64-bit rotate by a compile-time K as two 32-bit funnel shifts (SHF.L.W):
+// the generic form compiles to four shift/or instructions per rotate.
+template <int K>
+SABR_HD uint64_t rotl64c(uint64_t x) {
+#ifdef __CUDA_ARCH__
+    uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+    if constexpr (K >= 32) {
+        const uint32_t t = lo;
+        lo = hi;
+        hi = t;
+    }
+    constexpr int k = K & 31;
+    const uint32_t nhi = __funnelshift_l(lo, hi, k), nlo = __funnelshift_l(hi, lo, k);
+    return (static_cast<uint64_t>(nhi) << 32) | nlo;
+#else
+    return rotl64(x, K);
+#endif
+}
+
 // Xoshiro256pp, rng.hpp:16-43; state kept in four registers.
 struct Xoshiro {
     uint64_t s0, s1, s2, s3;
@@ -48,16 +67,20 @@ struct Xoshiro {
         s1 ^= s2;
         s0 ^= s3;
         s2 ^= t;
-        s3 = rotl64(s3, 45);
+        s3 = rotl64c<45>(s3);
     }
     // next(), rng.hpp:29-39
     SABR_HD uint64_t next() {
-        const uint64_t result = rotl64(s0 + s3, 23) + s0;
+        const uint64_t result = rotl64c<23>(s0 + s3) + s0;
         advance();
         return result;
     }
     // uniform(), rng.hpp:42: (next() >> 11) * 2^-53 (exact conversion)
     SABR_HD double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    // 2*uniform() - 1 (annealer.cpp:66) in one exact FMA: (n >> 11) * 2^-52
+    // is exact and the difference with 1 is representable, so this equals
+    // the reference's RN(RN(2u) - 1) bit for bit.
+    SABR_HD double sym() { return fma(static_cast<double>(next() >> 11), 0x1.0p-52, -1.0); }
 
     // state <- M^k state, where x^k mod P(x) = sum_i poly_i x^i (256 bits,
     // host-computed; see xoshiro_jump.cpp).  Branch-free masked accumulate.

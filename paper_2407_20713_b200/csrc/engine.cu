@@ -221,6 +221,8 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
         a.lo[i] = lo[i];
         a.hi[i] = hi[i];
         a.range[i] = hi[i] - lo[i];
+        a.lo2[i] = 2.0 * lo[i];
+        a.hi2[i] = 2.0 * hi[i];
     }
     a.free_mask = free_mask;
     a.dim_full = dim_full;

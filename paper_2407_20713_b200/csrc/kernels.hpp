@@ -33,6 +33,8 @@ struct SaLevelArgs {
     double lo[SABR_MAX_DIM];
     double hi[SABR_MAX_DIM];
     double range[SABR_MAX_DIM];  // hi - lo (annealer.cpp:65)
+    double lo2[SABR_MAX_DIM];    // 2*lo, 2*hi (the reflections of annealer.cpp:68-71,
+    double hi2[SABR_MAX_DIM];    // rounded on the host exactly as the reference does)
     uint32_t free_mask;          // bit i: full-vector dim i is searched
     int32_t dim_full;
     int32_t chain_length;
@@ -72,7 +74,8 @@ cudaError_t launch_vol_batch(int kind, const SurfaceView& sv, const double* para
 cudaError_t launch_case2_feasible(const double* params, int64_t n, uint8_t* out,
                                   cudaStream_t s);
 
-int sa_block_threads();
+int sa_block_threads();   // threads per CTA of the T_I level kernel (one record each)
+int t2_block_threads();   // threads per CTA of t2_level_end
 
 // ----------------------------------------------------------- T_II chains ---
 // Chain state of the Monte Carlo objective annealer, kept in HBM between the

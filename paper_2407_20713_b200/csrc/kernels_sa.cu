@@ -25,8 +25,14 @@ using namespace sabr_dev;
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
 constexpr size_t kSmemStageLimit = 96 * 1024;
+
+// Thread-per-chain level kernel: 64-thread CTAs, 11 per SM (22 warps, <= 88
+// registers).  1e5 chains = 1563 CTAs fit one wave on 148 SMs with at most
+// 22 warps per SM (128-thread CTAs: 6 per SM, 24 warps on the busiest SMs
+// and only 80 registers).
+constexpr int kLevelThreads = 64;
+constexpr int kLevelMinCtas = 11;
 
 // Per-quote market data as one 32-byte record (two LDS.128 per quote).
 struct __align__(16) Quote {
@@ -152,6 +158,160 @@ __device__ __forceinline__ double case1_cost(const double* v, const Grid& g) {
     return sum;
 }
 
+// ---------------------------------------- padded SoA grid (shared memory) ---
+// The objectives of the SA level kernel and the cost batch read the market
+// grid from shared memory as three arrays {ln(K/f), ln^2(K/f), 1/market},
+// each slice padded to a multiple of 4 quotes, so one quad of quotes is six
+// LDS.128 and the per-quote work is four FP64 instructions:
+//     s = C0 + A1*lm + A2*lm2   (C0, A1, A2 = c0, a1, a2 times 1/omega)
+//     r = 1 - s*(1/market)      (= (market - sigma)/market, calibration.cpp:262)
+//     acc += r*r
+// The last, partial quad of a slice is evaluated on the zero padding and its
+// padding lanes are discarded (predicated accumulate), so the padding never
+// enters a sum.
+struct PGrid {
+    int ns;
+    const double* T;
+    const double* lnf_hi;
+    const double* lnf_lo;
+    const int32_t* p0;  // [ns] first padded index of slice s (multiple of 4)
+    const int32_t* nq;  // [ns] quotes of slice s
+    const double* lm;   // [np]
+    const double* lm2;  // [np]
+    const double* inv;  // [np]
+    const double2* tab;
+};
+
+__host__ __device__ inline int padded_quotes(int ns, int nq) { return nq + 3 * ns; }
+
+__host__ __device__ inline size_t pstage_bytes(int ns, int nq) {
+    return 3 * sizeof(double) * padded_quotes(ns, nq) + 3 * sizeof(double) * ns +
+           2 * sizeof(int32_t) * ns + 16;
+}
+
+__device__ PGrid stage_pgrid(const SurfaceView& sv, unsigned char* smem) {
+    const int ns = sv.n_slices, npmax = padded_quotes(ns, sv.n_quotes);
+    double* lm = reinterpret_cast<double*>(smem);
+    double* lm2 = lm + npmax;
+    double* inv = lm2 + npmax;
+    double* d = inv + npmax;
+    int32_t* p0 = reinterpret_cast<int32_t*>(d + 3 * ns);
+    int32_t* nq = p0 + ns;
+    const Quote* src = reinterpret_cast<const Quote*>(sv.quotes);
+    int p = 0;
+    for (int s = 0; s < ns; ++s) {
+        const int q0 = sv.qoff[s], n = sv.qoff[s + 1] - q0, n4 = (n + 3) & ~3;
+        for (int k = threadIdx.x; k < n4; k += blockDim.x) {
+            const bool real = k < n;
+            const Quote q = real ? src[q0 + k] : Quote{0.0, 0.0, 0.0, 0.0};
+            lm[p + k] = q.lm;
+            lm2[p + k] = q.lm2;
+            inv[p + k] = q.inv_mkt;
+        }
+        if (threadIdx.x == 0) {
+            p0[s] = p;
+            nq[s] = n;
+            d[s] = sv.T[s];
+            d[ns + s] = sv.lnf_hi[s];
+            d[2 * ns + s] = sv.lnf_lo[s];
+        }
+        p += n4;
+    }
+    __syncthreads();
+    PGrid g;
+    g.ns = ns;
+    g.T = d;
+    g.lnf_hi = d + ns;
+    g.lnf_lo = d + 2 * ns;
+    g.p0 = p0;
+    g.nq = nq;
+    g.lm = lm;
+    g.lm2 = lm2;
+    g.inv = inv;
+    g.tab = nullptr;
+    return g;
+}
+
+struct QuadTerms {
+    double c0, a1, a2;
+};
+
+__device__ __forceinline__ QuadTerms quad_terms(const SmileTerms& t) {
+    return QuadTerms{t.c0 * t.inv_omega, t.a1 * t.inv_omega, t.a2 * t.inv_omega};
+}
+
+__device__ __forceinline__ double quad_rel(const QuadTerms& t, double lm, double lm2, double inv) {
+    return fma(-fma(t.a2, lm2, fma(t.a1, lm, t.c0)), inv, 1.0);
+}
+
+// Sum of squared relative errors over slice s (calibration.cpp:253-267),
+// four partial sums by quote index mod 4 (see slice_cost).
+__device__ __forceinline__ double pslice_cost(const SmileTerms& st, const PGrid& g, int s) {
+    const QuadTerms t = quad_terms(st);
+    const int p0 = g.p0[s], n = g.nq[s];
+    const double2* lm = reinterpret_cast<const double2*>(g.lm + p0);
+    const double2* lm2 = reinterpret_cast<const double2*>(g.lm2 + p0);
+    const double2* inv = reinterpret_cast<const double2*>(g.inv + p0);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int full = n >> 2;
+    int k = 0;
+#pragma unroll 1
+    for (; k < full; ++k) {
+        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
+        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
+        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
+        const double r0 = quad_rel(t, la.x, ma.x, ia.x), r1 = quad_rel(t, la.y, ma.y, ia.y);
+        const double r2 = quad_rel(t, lb.x, mb.x, ib.x), r3 = quad_rel(t, lb.y, mb.y, ib.y);
+        s0 = fma(r0, r0, s0);
+        s1 = fma(r1, r1, s1);
+        s2 = fma(r2, r2, s2);
+        s3 = fma(r3, r3, s3);
+    }
+    const int rem = n & 3;
+    if (rem) {
+        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
+        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
+        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
+        const double r0 = quad_rel(t, la.x, ma.x, ia.x), r1 = quad_rel(t, la.y, ma.y, ia.y);
+        const double r2 = quad_rel(t, lb.x, mb.x, ib.x);
+        s0 = fma(r0, r0, s0);
+        if (rem > 1) s1 = fma(r1, r1, s1);
+        if (rem > 2) s2 = fma(r2, r2, s2);
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
+__device__ __forceinline__ double static_cost(const double* v, const PGrid& g) {
+    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
+    const SmileTerms t = static_terms(v[0], v[1], v[2], v[3], pw, g.T[0]);
+    return pslice_cost(t, g, 0);
+}
+
+__device__ __forceinline__ double case1_cost(const double* v, const PGrid& g) {
+    double sum = 0.0;
+    const double omb = 1.0 - v[1];
+    for (int i = 0; i < g.ns; ++i) {
+        const double T = g.T[i];
+        double n1, n2, e1, e2;
+        dyn_coeffs_case1(v[2], v[3], v[4], v[5], T, n1, n2, e1, e2);
+        const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+        const SmileTerms t = dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, T);
+        sum += pslice_cost(t, g, i);
+    }
+    return sum;
+}
+
+// Objective grid of the SA / cost kernels: the padded SoA grid when it fits
+// in shared memory, else the AoS grid read through L1.
+template <bool SMEM>
+using ObjGrid = std::conditional_t<SMEM, PGrid, Grid>;
+
+template <bool SMEM>
+__device__ __forceinline__ ObjGrid<SMEM> stage_obj(const SurfaceView& sv, unsigned char* smem) {
+    if constexpr (SMEM) return stage_pgrid(sv, smem);
+    else return stage_grid<false>(sv, smem);
+}
+
 __device__ __forceinline__ double sq(double x) { return x * x; }
 
 // The closed-form objectives of proj/tests/test_annealer.cpp.
@@ -172,9 +332,8 @@ __device__ double builtin_value(int id, const double* x) {
     return CUDART_NAN;
 }
 
-template <int KIND, int NQ>
-__device__ __forceinline__ double objective(const double* v, const Grid& g, const SurfaceView& sv,
-                                            int builtin) {
+template <int KIND, class G>
+__device__ __forceinline__ double objective(const double* v, const G& g, int builtin) {
     if constexpr (KIND == OBJ_STATIC) return static_cost(v, g);
     else if constexpr (KIND == OBJ_CASE1) return case1_cost(v, g);
     else return builtin_value(builtin, v);
@@ -216,9 +375,11 @@ __device__ __forceinline__ long long warp_sum(long long x) {
     return x;
 }
 
+template <int NT>
 struct RedShared {
-    ArgMin e[kWarps], b[kWarps];
-    long long n[kWarps];
+    static constexpr int kW = NT / 32;
+    ArgMin e[kW], b[kW];
+    long long n[kW];
     ArgMin e_win, b_win;
     long long n_tot;
     int is_last;
@@ -226,7 +387,8 @@ struct RedShared {
 
 // Block-wide (endpoint, best) arg-min and eval sum; result valid in `rs`
 // after the call for all threads.
-__device__ void block_reduce(RedShared& rs, ArgMin e, ArgMin b, long long n) {
+template <int NT>
+__device__ void block_reduce(RedShared<NT>& rs, ArgMin e, ArgMin b, long long n) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     e = warp_argmin(e);
     b = warp_argmin(b);
@@ -240,7 +402,7 @@ __device__ void block_reduce(RedShared& rs, ArgMin e, ArgMin b, long long n) {
     if (threadIdx.x == 0) {
         ArgMin ee = rs.e[0], bb = rs.b[0];
         long long nn = rs.n[0];
-        for (int w = 1; w < kWarps; ++w) {
+        for (int w = 1; w < RedShared<NT>::kW; ++w) {
             argmin_combine(ee, rs.e[w]);
             argmin_combine(bb, rs.b[w]);
             nn += rs.n[w];
@@ -252,106 +414,11 @@ __device__ void block_reduce(RedShared& rs, ArgMin e, ArgMin b, long long n) {
     __syncthreads();
 }
 
-// --------------------------------------------------------- level kernel ---
-// Min CTAs/SM: 1e5 chains = 782 CTAs of 128 must fit ONE wave on 148 SMs
-// (6 CTAs/SM -> <= 85 registers); Case I carries more live state.
-template <int KIND>
-constexpr int level_min_ctas() { return 6; }
-
-template <int KIND, int DIMF, int NQ, bool SMEM>
-__global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
-    sa_level_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
-                    const int64_t level, const double temp) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ RedShared rs;
-    __shared__ sabr_level_record rec;
-
-    __shared__ double2 tab_s[kExpTableSize];
-
-    sabr_sa_state* st = a.state;
-    if (st->done) return;  // early-stopped run (max_evals): uniform exit
-
-    stage_exp(sv, tab_s);
-    Grid g{};
-    if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
-    __syncthreads();
-    g.tab = tab_s;
-
-    const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-    const bool active = local < a.n_local;
-    const int64_t chain = a.chain_begin + local;
-
-    // the chain-best point is written only on improvement and read once at
-    // the end: it lives in shared memory (column per thread), not registers
-    __shared__ double bp_s[DIMF][kThreads];
-    double* const bp = &bp_s[0][threadIdx.x];  // bp[i * kThreads] = dim i
-    double x[DIMF], y[DIMF];
-#pragma unroll
-    for (int i = 0; i < DIMF; ++i) {
-        x[i] = st->incumbent[i];
-        bp[i * kThreads] = x[i];
-    }
-    double fx = st->incumbent_value;
-    double bv = fx;
-    long long ev = 0;
-    const long long cap = st->eval_cap;
-
-    if (active) {
-        // substream keyed by (seed, level, chain): annealer.cpp:112-115
-        Xoshiro rng;
-        rng.init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain));
-        const double ratio = temp / a.t0;
-        const double scale = (ratio < 1.0) ? ratio : 1.0;  // std::min(1.0, T/t0), annealer.cpp:62
-        for (int step = 0; step < a.chain_length; ++step) {
-            if (ev >= cap) break;  // annealer.cpp:120
-            // propose, annealer.cpp:60-74 (no FMA contraction: bit-identical proposals)
-#pragma unroll
-            for (int i = 0; i < DIMF; ++i) {
-                if ((a.free_mask >> i) & 1u) {
-                    const double u = rng.uniform();
-                    const double stp =
-                        __dmul_rn(__dmul_rn(a.range[i], scale), __dsub_rn(__dmul_rn(2.0, u), 1.0));
-                    double v = __dadd_rn(x[i], stp);
-                    if (v > a.hi[i]) v = __dsub_rn(__dmul_rn(2.0, a.hi[i]), v);
-                    if (v < a.lo[i]) v = __dsub_rn(__dmul_rn(2.0, a.lo[i]), v);
-                    y[i] = (v < a.lo[i]) ? a.lo[i] : (a.hi[i] < v) ? a.hi[i] : v;
-                } else {
-                    y[i] = x[i];
-                }
-            }
-            if (!predicate_ok(a.predicate, y)) continue;  // annealer.cpp:122
-            double fy = objective<KIND, NQ>(y, g, sv, a.builtin);
-            if (isnan(fy)) fy = CUDART_INF;  // safe_eval, annealer.cpp:84-87
-            ++ev;
-            // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx)
-            bool accept = fy <= fx;
-            if (!accept) accept = rng.uniform() < exp_tab(-(fy - fx) / temp, tab_s);
-            if (accept) {
-#pragma unroll
-                for (int i = 0; i < DIMF; ++i) x[i] = y[i];
-                fx = fy;
-                if (fx < bv) {
-                    bv = fx;
-#pragma unroll
-                    for (int i = 0; i < DIMF; ++i) bp[i * kThreads] = x[i];
-                }
-            }
-        }
-    }
-
-    // ---- level-end reduction (annealer.cpp:141-159) ----
-    ArgMin e{active ? fx : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
-    ArgMin b{active ? bv : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
-    block_reduce(rs, e, b, ev);
-    if (active && chain == rs.e_win.i) {
-#pragma unroll
-        for (int i = 0; i < DIMF; ++i) rec.end_point[i] = x[i];
-    }
-    if (active && chain == rs.b_win.i) {
-#pragma unroll
-        for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp[i * kThreads];
-    }
-    __syncthreads();
+// One CTA record of the level-end reduction: written by thread 0, then the
+// ticket; returns true (all threads) in the last CTA of the grid.
+template <int NT, int DIMF>
+__device__ bool publish_block_record(RedShared<NT>& rs, sabr_level_record& rec,
+                                     const SaLevelArgs& a) {
     if (threadIdx.x == 0) {
         rec.end_value = rs.e_win.v;
         rec.end_chain = rs.e_win.i == LLONG_MAX ? -1 : rs.e_win.i;
@@ -364,21 +431,43 @@ __global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
         rs.is_last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (!rs.is_last) return;
+    return rs.is_last != 0;
+}
 
-    // ---- last CTA: reduce the CTA records of this rank ----
+// Last CTA: reduce the CTA records of this rank into the rank record and, on
+// a single rank, merge it into the annealer state (annealer.cpp:141-159).
+// Four records in flight per thread: the scan is L2-latency bound.
+template <int NT, int DIMF>
+__device__ void reduce_block_records(RedShared<NT>& rs, const SaLevelArgs& a, int64_t level) {
     __threadfence();
     ArgMin ee{CUDART_INF, LLONG_MAX, -1}, bb{CUDART_INF, LLONG_MAX, -1};
     long long nn = 0;
-    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += kThreads) {
-        const sabr_level_record* r = a.block_recs + k;
-        const double rev = __ldcg(&r->end_value);
-        const long long rei = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
-        const double rbv = __ldcg(&r->best_value);
-        const long long rbi = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
-        if (rei >= 0) argmin_combine(ee, ArgMin{rev, rei, k});
-        if (rbi >= 0) argmin_combine(bb, ArgMin{rbv, rbi, k});
-        nn += __ldcg(reinterpret_cast<const long long*>(&r->evals));
+    const int nrec = static_cast<int>(gridDim.x);
+    for (int k0 = threadIdx.x; k0 < nrec; k0 += 4 * NT) {
+        double rev[4], rbv[4];
+        long long rei[4], rbi[4], rn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u * NT;
+            rei[u] = rbi[u] = -1;
+            rn[u] = 0;
+            rev[u] = rbv[u] = CUDART_INF;
+            if (k < nrec) {
+                const sabr_level_record* r = a.block_recs + k;
+                rev[u] = __ldcg(&r->end_value);
+                rei[u] = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
+                rbv[u] = __ldcg(&r->best_value);
+                rbi[u] = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
+                rn[u] = __ldcg(reinterpret_cast<const long long*>(&r->evals));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u * NT;
+            if (rei[u] >= 0) argmin_combine(ee, ArgMin{rev[u], rei[u], k});
+            if (rbi[u] >= 0) argmin_combine(bb, ArgMin{rbv[u], rbi[u], k});
+            nn += rn[u];
+        }
     }
     block_reduce(rs, ee, bb, nn);
     if (threadIdx.x == 0) {
@@ -398,9 +487,126 @@ __global__ void __launch_bounds__(kThreads, level_min_ctas<KIND>())
         *a.rank_rec = out;
         *a.ticket = 0u;
         if (a.nranks == 1)
-            merge_level(st, &out, 1, a.n_chains, a.max_evals, a.levels_total, DIMF,
+            merge_level(a.state, &out, 1, a.n_chains, a.max_evals, a.levels_total, DIMF,
                         a.trace_f + level);
     }
+}
+
+// --------------------------------------------------------- level kernel ---
+// propose, annealer.cpp:60-74, for one coordinate: bit-identical to the
+// reference (2u - 1 via Xoshiro::sym, the reflections use the host-doubled
+// bounds, no FMA contraction).
+__device__ __forceinline__ double propose_coord(double x, double step_scale, double lo, double hi,
+                                                double lo2, double hi2, Xoshiro& rng) {
+    double v = __dadd_rn(x, __dmul_rn(step_scale, rng.sym()));
+    if (v > hi) v = __dsub_rn(hi2, v);
+    if (v < lo) v = __dsub_rn(lo2, v);
+    return (v < lo) ? lo : (hi < v) ? hi : v;
+}
+
+// One temperature level of this rank's chains (annealer.cpp:99-161).
+// ALLFREE: every coordinate is searched (no per-coordinate mask test).
+template <int KIND, int DIMF, bool ALLFREE, bool SMEM>
+__global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
+    sa_level_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
+                    const int64_t level, const double temp, const double inv_temp) {
+    constexpr int NT = kLevelThreads;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RedShared<NT> rs;
+    __shared__ sabr_level_record rec;
+    __shared__ double2 tab_s[kExpTableSize];
+    // the chain-best point is written only on improvement and read once at
+    // the end: it lives in shared memory (column per thread), not registers
+    __shared__ double bp_s[DIMF][NT];
+
+    sabr_sa_state* st = a.state;
+    if (st->done) return;  // early-stopped run (max_evals): uniform exit
+
+    stage_exp(sv, tab_s);
+    ObjGrid<SMEM> g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<SMEM>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
+
+    const int64_t local = static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x;
+    const bool active = local < a.n_local;
+    const int64_t chain = a.chain_begin + local;
+
+    double* const bp = &bp_s[0][threadIdx.x];  // bp[i * NT] = dim i
+    double x[DIMF], y[DIMF];
+#pragma unroll
+    for (int i = 0; i < DIMF; ++i) {
+        x[i] = st->incumbent[i];
+        bp[i * NT] = x[i];
+    }
+    double fx = st->incumbent_value;
+    double bv = fx;
+    int ev = 0;
+
+    if (active) {
+        // per-level eval cap (annealer.cpp:102-104) as a step count bound
+        const long long cap64 = st->eval_cap;
+        const int cap = cap64 < a.chain_length ? static_cast<int>(cap64 < 0 ? 0 : cap64) : a.chain_length;
+        // substream keyed by (seed, level, chain): annealer.cpp:112-115
+        Xoshiro rng;
+        rng.init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain));
+        const double ratio = temp / a.t0;
+        const double scale = (ratio < 1.0) ? ratio : 1.0;  // std::min(1.0, T/t0), annealer.cpp:62
+        double step_scale[DIMF];
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) step_scale[i] = __dmul_rn(a.range[i], scale);
+        for (int step = 0; step < a.chain_length; ++step) {
+            if (ev >= cap) break;  // annealer.cpp:120
+#pragma unroll
+            for (int i = 0; i < DIMF; ++i) {
+                if (ALLFREE || ((a.free_mask >> i) & 1u))
+                    y[i] = propose_coord(x[i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i], a.hi2[i], rng);
+                else
+                    y[i] = x[i];
+            }
+            if (!predicate_ok(a.predicate, y)) continue;  // annealer.cpp:122
+            double fy = objective<KIND>(y, g, a.builtin);
+            if (isnan(fy)) fy = CUDART_INF;  // safe_eval, annealer.cpp:84-87
+            ++ev;
+            // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx).
+            // (fy - fx) / T with the host's RN(1/T) and one exact-residual
+            // correction: the correctly rounded quotient (Markstein), without
+            // the IEEE division's special-case path.
+            bool accept = fy <= fx;
+            if (!accept) {
+                const double d = fy - fx;
+                const double q0 = d * inv_temp;
+                const double q = fma(fma(-q0, temp, d), inv_temp, q0);
+                accept = rng.uniform() < exp_tab(-q, tab_s);
+            }
+            if (accept) {
+#pragma unroll
+                for (int i = 0; i < DIMF; ++i) x[i] = y[i];
+                fx = fy;
+                if (fx < bv) {
+                    bv = fx;
+#pragma unroll
+                    for (int i = 0; i < DIMF; ++i) bp[i * NT] = x[i];
+                }
+            }
+        }
+    }
+
+    // ---- level-end reduction (annealer.cpp:141-159) ----
+    ArgMin e{active ? fx : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    ArgMin b{active ? bv : CUDART_INF, active ? chain : LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    block_reduce(rs, e, b, static_cast<long long>(ev));
+    if (active && chain == rs.e_win.i) {
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) rec.end_point[i] = x[i];
+    }
+    if (active && chain == rs.b_win.i) {
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp[i * NT];
+    }
+    __syncthreads();
+    if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
+    reduce_block_records<NT, DIMF>(rs, a, level);
 }
 
 __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* recs,
@@ -410,33 +616,33 @@ __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* re
                 a.trace_f + level);
 }
 
-template <int KIND, int DIMF, int NQ, bool SMEM>
+template <int KIND, int DIMF, bool SMEM>
 __global__ void sa_start_kernel(const __grid_constant__ SurfaceView sv, const SaLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 tab_s[kExpTableSize];
     stage_exp(sv, tab_s);
-    Grid g{};
-    if constexpr (KIND != OBJ_BUILTIN && NQ == 0) g = stage_grid<SMEM>(sv, smem);
+    ObjGrid<SMEM> g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<SMEM>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
     if (threadIdx.x != 0) return;
     double x[DIMF];
     for (int i = 0; i < DIMF; ++i) x[i] = a.state->incumbent[i];
-    double v = objective<KIND, NQ>(x, g, sv, a.builtin);
+    double v = objective<KIND>(x, g, a.builtin);
     if (isnan(v)) v = CUDART_INF;
     a.state->incumbent_value = v;
     a.state->best_value = v;
 }
 
-template <int KIND, int DIMF, int NQ, bool SMEM>
+// The SA objective on a batch of full parameter vectors (same code path).
+template <int KIND, int DIMF, bool SMEM>
 __global__ void __launch_bounds__(kThreads)
     cost_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
                       const int64_t n, double* __restrict__ cost) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 tab_s[kExpTableSize];
     stage_exp(sv, tab_s);
-    Grid g{};
-    if constexpr (NQ == 0) g = stage_grid<SMEM>(sv, smem);
+    ObjGrid<SMEM> g = stage_obj<SMEM>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
@@ -444,7 +650,7 @@ __global__ void __launch_bounds__(kThreads)
     double v[DIMF];
 #pragma unroll
     for (int k = 0; k < DIMF; ++k) v[k] = params[i * DIMF + k];
-    cost[i] = objective<KIND, NQ>(v, g, sv, 0);
+    cost[i] = objective<KIND>(v, g, 0);
 }
 
 // Model vols for every quote of the view (report rows, calibration.cpp:180-194).
@@ -626,10 +832,9 @@ __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs 
 
 __global__ void __launch_bounds__(kThreads)
     t2_level_end_kernel(const T2Chain* __restrict__ chains, const SaLevelArgs a, const int64_t level) {
-    __shared__ RedShared rs;
+    __shared__ RedShared<kThreads> rs;
     __shared__ sabr_level_record rec;
-    sabr_sa_state* st = a.state;
-    if (st->done) return;
+    if (a.state->done) return;
     const int64_t local = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const bool active = local < a.n_local;
     const int64_t chain = a.chain_begin + local;
@@ -642,55 +847,14 @@ __global__ void __launch_bounds__(kThreads)
     if (active && chain == rs.b_win.i)
         for (int i = 0; i < SABR_MAX_DIM; ++i) rec.best_point[i] = ch->bp[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        rec.end_value = rs.e_win.v;
-        rec.end_chain = rs.e_win.i == LLONG_MAX ? -1 : rs.e_win.i;
-        rec.best_value = rs.b_win.v;
-        rec.best_chain = rs.b_win.i == LLONG_MAX ? -1 : rs.b_win.i;
-        rec.evals = rs.n_tot;
-        a.block_recs[blockIdx.x] = rec;
-        __threadfence();
-        const unsigned t = atomicAdd(a.ticket, 1u);
-        rs.is_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!rs.is_last) return;
-    __threadfence();
-    ArgMin ee{CUDART_INF, LLONG_MAX, -1}, bb{CUDART_INF, LLONG_MAX, -1};
-    long long nn = 0;
-    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += kThreads) {
-        const sabr_level_record* r = a.block_recs + k;
-        const double rev = __ldcg(&r->end_value);
-        const long long rei = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
-        const double rbv = __ldcg(&r->best_value);
-        const long long rbi = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
-        if (rei >= 0) argmin_combine(ee, ArgMin{rev, rei, k});
-        if (rbi >= 0) argmin_combine(bb, ArgMin{rbv, rbi, k});
-        nn += __ldcg(reinterpret_cast<const long long*>(&r->evals));
-    }
-    block_reduce(rs, ee, bb, nn);
-    if (threadIdx.x == 0) {
-        sabr_level_record out;
-        out.end_value = rs.e_win.v;
-        out.end_chain = rs.e_win.blk >= 0 ? rs.e_win.i : -1;
-        out.best_value = rs.b_win.v;
-        out.best_chain = rs.b_win.blk >= 0 ? rs.b_win.i : -1;
-        out.evals = rs.n_tot;
-        out._pad = 0;
-        for (int i = 0; i < SABR_MAX_DIM; ++i) {
-            out.end_point[i] = rs.e_win.blk >= 0 ? __ldcg(&a.block_recs[rs.e_win.blk].end_point[i]) : 0.0;
-            out.best_point[i] = rs.b_win.blk >= 0 ? __ldcg(&a.block_recs[rs.b_win.blk].best_point[i]) : 0.0;
-        }
-        *a.rank_rec = out;
-        *a.ticket = 0u;
-        if (a.nranks == 1)
-            merge_level(st, &out, 1, a.n_chains, a.max_evals, a.levels_total, SABR_MAX_DIM,
-                        a.trace_f + level);
-    }
+    if (!publish_block_record<kThreads, SABR_MAX_DIM>(rs, rec, a)) return;
+    reduce_block_records<kThreads, SABR_MAX_DIM>(rs, a, level);
 }
 
-size_t smem_for(const SurfaceView& sv, int* use_smem) {
-    const size_t b = stage_bytes(sv.n_slices, sv.n_quotes);
+// Shared-memory bytes of the staged grid (0 and *use_smem = 0: read the AoS
+// grid through L1).  `padded`: the SoA layout of the SA / cost objectives.
+size_t smem_for(const SurfaceView& sv, int* use_smem, bool padded = false) {
+    const size_t b = padded ? pstage_bytes(sv.n_slices, sv.n_quotes) : stage_bytes(sv.n_slices, sv.n_quotes);
     *use_smem = b <= kSmemStageLimit;
     return *use_smem ? b : 0;
 }
@@ -703,67 +867,65 @@ cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaSuccess;
 }
 
-// Launch `body(kernel_ptr, smem_bytes)` for the SMEM variant the view
-// supports: the market grid staged in shared memory, or (too large) read
+// Run `body(kernel_ptr, smem_bytes)` with the SMEM variant the view supports:
+// the padded grid staged in shared memory, or (too large) the AoS grid read
 // through L1.  (Kernel-parameter/constant-bank grids were tried: sm_100a FP64
 // instructions take no constant-bank operands, so they only add registers.)
-template <int KIND, int DIMF, template <int, int, int, bool> class KSel, class Body>
-cudaError_t dispatch_grid(const SurfaceView& sv, Body&& body) {
+template <int KIND, class Pick, class Body>
+cudaError_t dispatch_grid(const SurfaceView& sv, Pick&& pick, Body&& body) {
     if constexpr (KIND == OBJ_BUILTIN) {
-        return body(KSel<KIND, DIMF, 0, true>::get(), size_t(0));
+        return body(pick(std::true_type{}), size_t(0));
     } else {
         int use = 0;
-        const size_t smem = smem_for(sv, &use);
-        if (use) return body(KSel<KIND, DIMF, 0, true>::get(), smem);
-        return body(KSel<KIND, DIMF, 0, false>::get(), size_t(0));
+        const size_t smem = smem_for(sv, &use, true);
+        if (use) return body(pick(std::true_type{}), smem);
+        return body(pick(std::false_type{}), size_t(0));
     }
 }
-
-template <int K, int D, int N, bool S>
-struct LevelSel {
-    static auto get() { return sa_level_kernel<K, D, N, S>; }
-};
-template <int K, int D, int N, bool S>
-struct StartSel {
-    static auto get() { return sa_start_kernel<K, D, N, S>; }
-};
-template <int K, int D, int N, bool S>
-struct CostSel {
-    static auto get() { return cost_batch_kernel<K, D, N, S>; }
-};
 
 template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
-    const unsigned grid = static_cast<unsigned>((a.n_local + kThreads - 1) / kThreads);
-    return dispatch_grid<KIND, DIMF, LevelSel>(sv, [&](auto k, size_t smem) {
+    const unsigned grid = static_cast<unsigned>((a.n_local + kLevelThreads - 1) / kLevelThreads);
+    const bool all_free = a.free_mask == (1u << DIMF) - 1u;
+    const double inv_temp = 1.0 / temp;
+    auto run = [&](auto k, size_t smem) {
         cudaError_t e = set_smem(k, smem);
         if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, smem, s>>>(sv, a, level, temp);
+        k<<<grid, kLevelThreads, smem, s>>>(sv, a, level, temp, inv_temp);
         return cudaGetLastError();
-    });
+    };
+    if (all_free)
+        return dispatch_grid<KIND>(
+            sv, [](auto smem) { return sa_level_kernel<KIND, DIMF, true, decltype(smem)::value>; }, run);
+    return dispatch_grid<KIND>(
+        sv, [](auto smem) { return sa_level_kernel<KIND, DIMF, false, decltype(smem)::value>; }, run);
 }
 
 template <int KIND, int DIMF>
 cudaError_t start_t(const SurfaceView& sv, const SaLevelArgs& a, cudaStream_t s) {
-    return dispatch_grid<KIND, DIMF, StartSel>(sv, [&](auto k, size_t smem) {
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<1, 32, smem, s>>>(sv, a);
-        return cudaGetLastError();
-    });
+    return dispatch_grid<KIND>(
+        sv, [](auto smem) { return sa_start_kernel<KIND, DIMF, decltype(smem)::value>; },
+        [&](auto k, size_t smem) {
+            cudaError_t e = set_smem(k, smem);
+            if (e != cudaSuccess) return e;
+            k<<<1, 32, smem, s>>>(sv, a);
+            return cudaGetLastError();
+        });
 }
 
 template <int KIND, int DIMF>
 cudaError_t cost_t(const SurfaceView& sv, const double* params, int64_t n, double* cost,
                    cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>((n + kThreads - 1) / kThreads);
-    return dispatch_grid<KIND, DIMF, CostSel>(sv, [&](auto k, size_t smem) {
-        cudaError_t e = set_smem(k, smem);
-        if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, smem, s>>>(sv, params, n, cost);
-        return cudaGetLastError();
-    });
+    return dispatch_grid<KIND>(
+        sv, [](auto smem) { return cost_batch_kernel<KIND, DIMF, decltype(smem)::value>; },
+        [&](auto k, size_t smem) {
+            cudaError_t e = set_smem(k, smem);
+            if (e != cudaSuccess) return e;
+            k<<<grid, kThreads, smem, s>>>(sv, params, n, cost);
+            return cudaGetLastError();
+        });
 }
 
 template <int KIND, int DIMF>
@@ -785,7 +947,8 @@ cudaError_t vol_t(const SurfaceView& sv, const double* params, int64_t n, double
 
 }  // namespace
 
-int sa_block_threads() { return kThreads; }
+int sa_block_threads() { return kLevelThreads; }
+int t2_block_threads() { return kThreads; }
 
 #define SABR_DISPATCH(kind, dim, CALL)                                       \
     do {                                                                     \

@@ -134,7 +134,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     a.n_chains = n_chains;
     a.max_evals = sch.max_evals;
     a.levels_total = L;
-    const int64_t grid = std::max<int64_t>(1, (n_local + sa_block_threads() - 1) / sa_block_threads());
+    const int64_t grid = std::max<int64_t>(1, (n_local + t2_block_threads() - 1) / t2_block_threads());
     a.state = static_cast<sabr_sa_state*>(dev_buf(ctx, "sa_state", sizeof(sabr_sa_state)));
     a.block_recs = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_block_recs", sizeof(sabr_level_record) * grid));
     a.rank_rec = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_rank_rec", sizeof(sabr_level_record)));
