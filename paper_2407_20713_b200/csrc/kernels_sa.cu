@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "device_common.cuh"
@@ -299,6 +300,89 @@ __device__ __forceinline__ double case1_cost(const double* v, const PGrid& g) {
         sum += pslice_cost(t, g, i);
     }
     return sum;
+}
+
+// ------------------------------------- C chains per thread (shared loads) ---
+// pslice_cost for C candidates at once: one set of quote loads feeds all C
+// (the per-candidate arithmetic and summation order are those of
+// pslice_cost, so each result is bit-identical to the single-chain path).
+template <int C>
+__device__ __forceinline__ void pslice_cost_n(const QuadTerms (&t)[C], const PGrid& g, int s,
+                                              double (&out)[C]) {
+    const int p0 = g.p0[s], n = g.nq[s];
+    const double2* lm = reinterpret_cast<const double2*>(g.lm + p0);
+    const double2* lm2 = reinterpret_cast<const double2*>(g.lm2 + p0);
+    const double2* inv = reinterpret_cast<const double2*>(g.inv + p0);
+    double acc[C][4];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0.0;
+    const int full = n >> 2;
+    int k = 0;
+#pragma unroll 1
+    for (; k < full; ++k) {
+        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
+        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
+        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const double r0 = quad_rel(t[c], la.x, ma.x, ia.x), r1 = quad_rel(t[c], la.y, ma.y, ia.y);
+            const double r2 = quad_rel(t[c], lb.x, mb.x, ib.x), r3 = quad_rel(t[c], lb.y, mb.y, ib.y);
+            acc[c][0] = fma(r0, r0, acc[c][0]);
+            acc[c][1] = fma(r1, r1, acc[c][1]);
+            acc[c][2] = fma(r2, r2, acc[c][2]);
+            acc[c][3] = fma(r3, r3, acc[c][3]);
+        }
+    }
+    const int rem = n & 3;
+    if (rem) {
+        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
+        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
+        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const double r0 = quad_rel(t[c], la.x, ma.x, ia.x), r1 = quad_rel(t[c], la.y, ma.y, ia.y);
+            const double r2 = quad_rel(t[c], lb.x, mb.x, ib.x);
+            acc[c][0] = fma(r0, r0, acc[c][0]);
+            if (rem > 1) acc[c][1] = fma(r1, r1, acc[c][1]);
+            if (rem > 2) acc[c][2] = fma(r2, r2, acc[c][2]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[c] = (acc[c][0] + acc[c][1]) + (acc[c][2] + acc[c][3]);
+}
+
+template <int C, int DIMF>
+__device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const PGrid& g,
+                                              double (&out)[C]) {
+    QuadTerms t[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
+        t[c] = quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, g.T[0]));
+    }
+    pslice_cost_n<C>(t, g, 0, out);
+}
+
+template <int C, int DIMF>
+__device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const PGrid& g,
+                                             double (&out)[C]) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[c] = 0.0;
+    for (int i = 0; i < g.ns; ++i) {
+        const double T = g.T[i];
+        QuadTerms t[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double n1, n2, e1, e2;
+            dyn_coeffs_case1(v[c][2], v[c][3], v[c][4], v[c][5], T, n1, n2, e1, e2);
+            const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            t[c] = quad_terms(dynamic_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T));
+        }
+        double s[C];
+        pslice_cost_n<C>(t, g, i, s);
+#pragma unroll
+        for (int c = 0; c < C; ++c) out[c] += s[c];
+    }
 }
 
 // Objective grid of the SA / cost kernels: the padded SoA grid when it fits
@@ -609,6 +693,135 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
     reduce_block_records<NT, DIMF>(rs, a, level);
 }
 
+// The same level with kCpt chains per thread (model objectives, grid in
+// shared memory, no predicate): the chains of a thread step in lockstep and
+// share the quote loads, the loop control and the constants, and their
+// independent dependency chains interleave (ILP).  A CTA of kPairThreads
+// threads covers kPairThreads * kCpt = kLevelThreads chains (thread t owns
+// chains t and t + kPairThreads of the CTA's range), so the per-CTA records
+// are those of sa_level_kernel.  Each chain's arithmetic is that of
+// sa_level_kernel: the two kernels produce identical trajectories.
+constexpr int kCpt = 2;
+constexpr int kPairThreads = kLevelThreads / kCpt;
+constexpr int kPairMinCtas = 11;  // 1e5 chains: 1563 CTAs of 32 threads in one wave
+
+template <int KIND, int DIMF, bool ALLFREE>
+__global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
+    sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
+                          const int64_t level, const double temp, const double inv_temp) {
+    constexpr int NT = kPairThreads;
+    constexpr int C = kCpt;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RedShared<NT> rs;
+    __shared__ sabr_level_record rec;
+    __shared__ double2 tab_s[kExpTableSize];
+    __shared__ double bp_s[C][DIMF][NT];
+
+    sabr_sa_state* st = a.state;
+    if (st->done) return;
+    stage_exp(sv, tab_s);
+    PGrid g = stage_pgrid(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
+
+    bool active[C];
+    int64_t chain[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int64_t local = static_cast<int64_t>(blockIdx.x) * (NT * C) + c * NT + threadIdx.x;
+        active[c] = local < a.n_local;
+        chain[c] = a.chain_begin + local;
+    }
+    double x[C][DIMF], y[C][DIMF], fx[C], bv[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) {
+            x[c][i] = st->incumbent[i];
+            bp_s[c][i][threadIdx.x] = x[c][i];
+        }
+        fx[c] = bv[c] = st->incumbent_value;
+    }
+    int steps = 0;
+    if (active[0]) {  // chain c > 0 active implies chain 0 active
+        const long long cap64 = st->eval_cap;
+        steps = cap64 < a.chain_length ? static_cast<int>(cap64 < 0 ? 0 : cap64) : a.chain_length;
+        Xoshiro rng[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
+        const double ratio = temp / a.t0;
+        const double scale = (ratio < 1.0) ? ratio : 1.0;
+        double step_scale[DIMF];
+#pragma unroll
+        for (int i = 0; i < DIMF; ++i) step_scale[i] = __dmul_rn(a.range[i], scale);
+        for (int step = 0; step < steps; ++step) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+#pragma unroll
+                for (int i = 0; i < DIMF; ++i) {
+                    if (ALLFREE || ((a.free_mask >> i) & 1u))
+                        y[c][i] = propose_coord(x[c][i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i],
+                                                a.hi2[i], rng[c]);
+                    else
+                        y[c][i] = x[c][i];
+                }
+            }
+            double fy[C];
+            if constexpr (KIND == OBJ_STATIC) static_cost_n<C, DIMF>(y, g, fy);
+            else case1_cost_n<C, DIMF>(y, g, fy);
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (isnan(fy[c])) fy[c] = CUDART_INF;
+                bool accept = fy[c] <= fx[c];
+                if (!accept) {
+                    const double d = fy[c] - fx[c];
+                    const double q0 = d * inv_temp;
+                    const double q = fma(fma(-q0, temp, d), inv_temp, q0);
+                    accept = rng[c].uniform() < exp_tab(-q, tab_s);
+                }
+                if (accept) {
+#pragma unroll
+                    for (int i = 0; i < DIMF; ++i) x[c][i] = y[c][i];
+                    fx[c] = fy[c];
+                    if (fx[c] < bv[c]) {
+                        bv[c] = fx[c];
+#pragma unroll
+                        for (int i = 0; i < DIMF; ++i) bp_s[c][i][threadIdx.x] = x[c][i];
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- level-end reduction (annealer.cpp:141-159) ----
+    ArgMin e{CUDART_INF, LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    ArgMin b{CUDART_INF, LLONG_MAX, static_cast<int32_t>(blockIdx.x)};
+    long long ev = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        if (!active[c]) continue;
+        argmin_combine(e, ArgMin{fx[c], chain[c], static_cast<int32_t>(blockIdx.x)});
+        argmin_combine(b, ArgMin{bv[c], chain[c], static_cast<int32_t>(blockIdx.x)});
+        ev += steps;
+    }
+    block_reduce(rs, e, b, ev);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        if (active[c] && chain[c] == rs.e_win.i) {
+#pragma unroll
+            for (int i = 0; i < DIMF; ++i) rec.end_point[i] = x[c][i];
+        }
+        if (active[c] && chain[c] == rs.b_win.i) {
+#pragma unroll
+            for (int i = 0; i < DIMF; ++i) rec.best_point[i] = bp_s[c][i][threadIdx.x];
+        }
+    }
+    __syncthreads();
+    if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
+    reduce_block_records<NT, DIMF>(rs, a, level);
+}
+
 __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* recs,
                                 const int64_t level) {
     if (a.state->done) return;
@@ -883,6 +1096,15 @@ cudaError_t dispatch_grid(const SurfaceView& sv, Pick&& pick, Body&& body) {
     }
 }
 
+// SABR_SA_CPT=1 selects the one-chain-per-thread level kernel (A/B checks).
+bool multi_chain_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SABR_SA_CPT");
+        return !(e && std::atoi(e) == 1);
+    }();
+    return on;
+}
+
 template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
@@ -895,6 +1117,17 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
         k<<<grid, kLevelThreads, smem, s>>>(sv, a, level, temp, inv_temp);
         return cudaGetLastError();
     };
+    if constexpr (KIND != OBJ_BUILTIN) {
+        int use = 0;
+        const size_t smem = smem_for(sv, &use, true);
+        if (use && multi_chain_enabled()) {
+            auto k = all_free ? sa_level_multi_kernel<KIND, DIMF, true> : sa_level_multi_kernel<KIND, DIMF, false>;
+            cudaError_t e = set_smem(k, smem);
+            if (e != cudaSuccess) return e;
+            k<<<grid, kPairThreads, smem, s>>>(sv, a, level, temp, inv_temp);
+            return cudaGetLastError();
+        }
+    }
     if (all_free)
         return dispatch_grid<KIND>(
             sv, [](auto smem) { return sa_level_kernel<KIND, DIMF, true, decltype(smem)::value>; }, run);

@@ -1,0 +1,59 @@
+"""The two T_I level kernels (one chain per thread, and kCpt chains per thread
+sharing the quote loads; kernels_sa.cu) must produce bit-identical annealer
+trajectories.  The one-chain kernel is selected with SABR_SA_CPT=1, read once
+per process, so each variant runs in its own subprocess."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+import paper_2407_20713_b200 as pkg
+eng = pkg.Engine(0)
+eq = pkg.parse_surface("tests/data/eurostoxx50.csv")
+fx = pkg.parse_surface("tests/data/eurusd.csv")
+out = {}
+# odd chain count: the last thread of the multi-chain kernel has an inactive chain
+s = pkg.AnnealingSchedule(t0=2.0, cooling=0.9, chain_length=60, workers=301, groups=3, t_min=1e-4, seed=5)
+r = eng.calibrate_static_T1(eq, 1, None, s, None, trace=True)
+out["static"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                 [f.hex() for _, f in r.temperature_trace]]
+r = eng.calibrate_static_T1(fx, 2, None, s, {"beta": 0.5}, trace=True)
+out["static_fixed"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                       [f.hex() for _, f in r.temperature_trace]]
+# eval cap reached inside a level
+s2 = pkg.AnnealingSchedule(t0=2.0, cooling=0.8, chain_length=50, workers=77, t_min=1e-2, seed=9, max_evals=20000)
+r = eng.calibrate_static_T1(fx, 0, None, s2, None, trace=True)
+out["static_cap"] = [r.final_cost.hex(), r.evals, [f.hex() for _, f in r.temperature_trace]]
+s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.8, chain_length=40, workers=129, t_min=1e-3, seed=2)
+r = eng.calibrate_dynamic_case1_T1(fx, None, s3, None, trace=True)
+out["case1"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                [f.hex() for _, f in r.temperature_trace]]
+print(json.dumps(out))
+"""
+
+
+def run_variant(cpt):
+    env = dict(os.environ)
+    env.pop("SABR_SA_CPT", None)
+    if cpt is not None:
+        env["SABR_SA_CPT"] = str(cpt)
+    p = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+def test_multi_chain_kernel_matches_single_chain_kernel():
+    multi = run_variant(None)
+    single = run_variant(1)
+    assert multi.keys() == single.keys()
+    for k in multi:
+        assert multi[k] == single[k], k

@@ -7,8 +7,8 @@ M=smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_exe
 for m in sa case1 t2 mc; do timeout 300 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_$m.csv python tools/profile_kernels.py $m > gpurun_out/prof_$m.log 2>&1; done
 SABR_MC_CB=4 timeout 300 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_t2_cb4.csv python tools/profile_kernels.py t2 > gpurun_out/prof_t2_cb4.log 2>&1
 if [ "${FULL:-1}" = "1" ]; then
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level_kernel -s 1 -c 1 -o gpurun_out/full_sa python tools/profile_kernels.py sa > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level_kernel -s 1 -c 1 -o gpurun_out/full_case1 python tools/profile_kernels.py case1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level -s 1 -c 1 -o gpurun_out/full_sa python tools/profile_kernels.py sa > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level -s 1 -c 1 -o gpurun_out/full_case1 python tools/profile_kernels.py case1 > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:mc_tile_kernel -s 2 -c 1 -o gpurun_out/full_t2 python tools/profile_kernels.py t2 > /dev/null 2>&1
 fi
 ls -la gpurun_out

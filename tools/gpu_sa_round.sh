@@ -5,5 +5,5 @@ timeout 600 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider -
 timeout 600 python bench.py --steps 2 --warmup 3 ${BENCH_ARGS:-} > gpurun_out/bench.log 2>&1
 M=smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread
 for m in sa case1; do timeout 300 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_$m.csv python tools/profile_kernels.py $m > gpurun_out/prof_$m.log 2>&1; done
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level_kernel -s 1 -c 1 -o gpurun_out/full_sa python tools/profile_kernels.py sa > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level -s 1 -c 1 -o gpurun_out/full_sa python tools/profile_kernels.py sa > /dev/null 2>&1
 ls -la gpurun_out

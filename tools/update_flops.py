@@ -22,10 +22,10 @@ def per(path, prefix, units, pick=-1):
             g["dram__bytes_read.sum"] + g["dram__bytes_write.sum"], g["gpu__time_duration.sum"])
 
 
-def main(tag):
+def main(tag, copy=("sa", "case1", "t2", "t2_cb4", "mc")):
     src = os.path.join(ROOT, "gpurun_out")
-    sa = per(os.path.join(src, "ncu_metrics_sa.csv"), "sa_level_kernel<0", 1e7)
-    c1 = per(os.path.join(src, "ncu_metrics_case1.csv"), "sa_level_kernel<1", 1e7)
+    sa = per(os.path.join(src, "ncu_metrics_sa.csv"), ("sa_level_multi_kernel<0", "sa_level_kernel<0"), 1e7)
+    c1 = per(os.path.join(src, "ncu_metrics_case1.csv"), ("sa_level_multi_kernel<1", "sa_level_kernel<1"), 1e7)
     t2 = per(os.path.join(src, "ncu_metrics_t2.csv"), "mc_tile_kernel<8", 32 * 1e5 * 250)
     mc = per(os.path.join(src, "ncu_metrics_mc.csv"), "mc_tile_kernel<1", (1 << 20) * 124)
     d = {"source": f"ncu smsp__sass_thread_inst_executed_op_{{dfma,dadd,dmul}}_pred_on.sum (DFMA = 2 FLOP) "
@@ -39,7 +39,7 @@ def main(tag):
          "mc_single_flops_per_path_step": mc[0], "mc_single_fp64_instr_per_path_step": mc[1]}
     with open(os.path.join(ROOT, "profiles", "fp64_per_eval.json"), "w") as f:
         json.dump(d, f, indent=1)
-    for m in ("sa", "case1", "t2", "t2_cb4", "mc"):
+    for m in copy:
         p = os.path.join(src, f"ncu_metrics_{m}.csv")
         if os.path.exists(p):
             shutil.copy(p, os.path.join(ROOT, "profiles", f"{tag}_ncu_metrics_{m}.csv"))
@@ -47,4 +47,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], *(sys.argv[2:3] and [sys.argv[2].split(",")]))
