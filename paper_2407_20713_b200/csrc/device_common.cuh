@@ -75,6 +75,10 @@ struct Xoshiro {
         advance();
         return result;
     }
+    // the uniform() that the next draw would return, without drawing it
+    SABR_HD double peek_uniform() const {
+        return static_cast<double>((rotl64c<23>(s0 + s3) + s0) >> 11) * 0x1.0p-53;
+    }
     // uniform(), rng.hpp:42: (next() >> 11) * 2^-53 (exact conversion)
     SABR_HD double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
     // 2*uniform() - 1 (annealer.cpp:66) in one exact FMA: (n >> 11) * 2^-52
@@ -154,7 +158,9 @@ SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, dou
 // long double (kernels_mc.cu: exp_table_host()).
 constexpr int kExpTableSize = 128;
 
-SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
+// exp_tab without the saturation test: valid for |x| <= 700 only (callers
+// that can bound the argument on the host use it and save the compare/select).
+SABR_D double exp_tab_unsat(double x, const double2* __restrict__ tab) {
     constexpr double kInvLn2N = 0x1.71547652b82fep7;  // 128 / ln 2
     constexpr double kShift = 0x1.8p52;
     constexpr double kLn2NHi = 0x1.62e42fefa39efp-8;  // ln2/128 = hi + lo (FMA reduction)
@@ -171,7 +177,11 @@ SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
     const double2 t = tab[k & 127];
     const double v = t.x + fma(t.x, p, t.y);
     // scale by 2^(k >> 7): add to the exponent field (result stays normal for |x| <= 700)
-    const double res = __hiloint2double(__double2hiint(v) + ((k >> 7) << 20), __double2loint(v));
+    return __hiloint2double(__double2hiint(v) + ((k >> 7) << 20), __double2loint(v));
+}
+
+SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
+    const double res = exp_tab_unsat(x, tab);
     // NaN fails the test and flows through the arithmetic into res
     const double sat = x > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
     return fabs(x) > 700.0 ? sat : res;

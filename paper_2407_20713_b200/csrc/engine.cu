@@ -170,6 +170,32 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 }
 
 // ---------------------------------------------------------- T_I annealer ---
+// True when every dim is free and, for every x in [lo, hi] and every step of
+// propose (annealer.cpp:60-74), the first reflection already lands in
+// [lo, hi].  The step is s = RN(RN(range*scale) * sym) with scale <= 1 and
+// sym = 2u - 1 in [-1, 1 - 2^-52], so -range <= s <= RN(range*(1 - 2^-52))
+// and (rounding is monotone) v = RN(x + s) lies in
+// [RN(lo - range), RN(hi + RN(range*(1 - 2^-52)))]; if 2hi - v >= lo and
+// 2lo - v <= hi hold at those extremes, the reference's second reflection and
+// its clamp never change the value, and the level kernels use
+// propose_coord_fast (same bits, fewer compares).
+bool single_reflection(const SaLevelArgs& a, int dim_full) {
+    static const bool enabled = [] {  // SABR_SA_FAST=0: general propose (A/B checks)
+        const char* e = std::getenv("SABR_SA_FAST");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (!enabled) return false;
+    for (int i = 0; i < dim_full; ++i) {
+        if (!((a.free_mask >> i) & 1u)) return false;
+        const double vmax = a.hi[i] + a.range[i] * (1.0 - 0x1.0p-52), vmin = a.lo[i] - a.range[i];
+        if (!std::isfinite(vmax) || !std::isfinite(vmin) || !std::isfinite(a.hi2[i]) ||
+            !std::isfinite(a.lo2[i]))
+            return false;
+        if (!(a.hi2[i] - vmax >= a.lo[i]) || !(a.lo2[i] - vmin <= a.hi[i])) return false;
+    }
+    return true;
+}
+
 struct T1Out {
     std::vector<double> best_full;
     double best_value = 0.0;
@@ -225,6 +251,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
         a.hi2[i] = 2.0 * hi[i];
     }
     a.free_mask = free_mask;
+    a.fast = single_reflection(a, dim_full) ? 1 : 0;
     a.dim_full = dim_full;
     a.chain_length = sch.chain_length;
     a.builtin = builtin;
@@ -715,6 +742,8 @@ SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& 
     v.lnf_lo = v.T + 2 * ns;
     v.qoff = dq;
     v.exptab = exp_table_device(ctx);
+    v.max_abs_lnf = 0.0;
+    for (int i = 0; i < ns; ++i) v.max_abs_lnf = std::max(v.max_abs_lnf, std::fabs(sd[ns + i]));
     return v;
 }
 

@@ -21,6 +21,7 @@ struct SurfaceView {
     // expression, evaluated on the host), lm*lm, market value, 1/market}
     const double* quotes;
     const double2* exptab;  // [128] exp_tab table (device_common.cuh), staged per CTA
+    double max_abs_lnf;     // max_i |ln f_i| (host-side bound for the unsaturated exp)
 };
 
 enum ObjectiveKind : int32_t {
@@ -41,6 +42,7 @@ struct SaLevelArgs {
     int32_t builtin;             // sabr_builtin_objective when OBJ_BUILTIN
     int32_t predicate;           // SABR_PRED_*
     int32_t nranks;
+    int32_t fast;                // all dims free and one reflection always lands in the box
     double t0;
     uint64_t seed;
     int64_t chain_begin;         // global index of this rank's first chain

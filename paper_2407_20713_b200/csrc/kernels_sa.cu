@@ -98,11 +98,13 @@ __device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem) {
 
 // f^(1-beta) = exp((1-beta) ln f) with ln f carried in double-double, so the
 // result is as accurate as a correctly rounded exp (pow in analytics.cpp:191).
+// SAT = false: |(1-beta) ln f| <= 700 is guaranteed by the host (FAST kernels).
+template <bool SAT = true>
 __device__ __forceinline__ double pow_fwd(double omb, double lnf_hi, double lnf_lo,
                                           const double2* tab) {
     const double y = omb * lnf_hi;
     const double err = fma(omb, lnf_hi, -y) + omb * lnf_lo;
-    const double e = exp_tab(y, tab);
+    const double e = SAT ? exp_tab(y, tab) : exp_tab_unsat(y, tab);
     return fma(e, err, e);
 }
 
@@ -159,55 +161,58 @@ __device__ __forceinline__ double case1_cost(const double* v, const Grid& g) {
     return sum;
 }
 
-// ---------------------------------------- padded SoA grid (shared memory) ---
+// ------------------------------------ padded quad grid (shared memory) ---
 // The objectives of the SA level kernel and the cost batch read the market
-// grid from shared memory as three arrays {ln(K/f), ln^2(K/f), 1/market},
-// each slice padded to a multiple of 4 quotes, so one quad of quotes is six
-// LDS.128 and the per-quote work is four FP64 instructions:
+// grid from shared memory as quad records: quotes 4k..4k+3 of a slice are
+// one 96-byte record {ln(K/f)[4], ln^2(K/f)[4], 1/market[4]}, each slice
+// padded to whole quads, so one quad is six LDS.128 at immediate offsets of
+// one base pointer and the per-quote work is four FP64 instructions:
 //     s = C0 + A1*lm + A2*lm2   (C0, A1, A2 = c0, a1, a2 times 1/omega)
 //     r = 1 - s*(1/market)      (= (market - sigma)/market, calibration.cpp:262)
 //     acc += r*r
 // The last, partial quad of a slice is evaluated on the zero padding and its
 // padding lanes are discarded (predicated accumulate), so the padding never
-// enters a sum.
+// enters a sum.  One extra zero quad ends the grid: the quad loop prefetches
+// the record after the one it computes.
+struct QuadRec {
+    double2 lm01, lm23, sq01, sq23, inv01, inv23;
+};
+
 struct PGrid {
     int ns;
     const double* T;
     const double* lnf_hi;
     const double* lnf_lo;
-    const int32_t* p0;  // [ns] first padded index of slice s (multiple of 4)
+    const int32_t* p0;  // [ns] first quad of slice s
     const int32_t* nq;  // [ns] quotes of slice s
-    const double* lm;   // [np]
-    const double* lm2;  // [np]
-    const double* inv;  // [np]
+    const QuadRec* rec;
     const double2* tab;
 };
 
-__host__ __device__ inline int padded_quotes(int ns, int nq) { return nq + 3 * ns; }
+__host__ __device__ inline int grid_quads(int ns, int nq) { return (nq + 3 * ns + 3) / 4 + 1; }
 
 __host__ __device__ inline size_t pstage_bytes(int ns, int nq) {
-    return 3 * sizeof(double) * padded_quotes(ns, nq) + 3 * sizeof(double) * ns +
-           2 * sizeof(int32_t) * ns + 16;
+    return sizeof(QuadRec) * grid_quads(ns, nq) + 3 * sizeof(double) * ns + 2 * sizeof(int32_t) * ns + 16;
 }
 
 __device__ PGrid stage_pgrid(const SurfaceView& sv, unsigned char* smem) {
-    const int ns = sv.n_slices, npmax = padded_quotes(ns, sv.n_quotes);
-    double* lm = reinterpret_cast<double*>(smem);
-    double* lm2 = lm + npmax;
-    double* inv = lm2 + npmax;
-    double* d = inv + npmax;
+    const int ns = sv.n_slices, nqd = grid_quads(ns, sv.n_quotes);
+    QuadRec* rec = reinterpret_cast<QuadRec*>(smem);
+    double* d = reinterpret_cast<double*>(rec + nqd);
     int32_t* p0 = reinterpret_cast<int32_t*>(d + 3 * ns);
     int32_t* nq = p0 + ns;
+    double* flat = reinterpret_cast<double*>(rec);
     const Quote* src = reinterpret_cast<const Quote*>(sv.quotes);
-    int p = 0;
+    int p = 0;  // quad index
     for (int s = 0; s < ns; ++s) {
         const int q0 = sv.qoff[s], n = sv.qoff[s + 1] - q0, n4 = (n + 3) & ~3;
         for (int k = threadIdx.x; k < n4; k += blockDim.x) {
             const bool real = k < n;
             const Quote q = real ? src[q0 + k] : Quote{0.0, 0.0, 0.0, 0.0};
-            lm[p + k] = q.lm;
-            lm2[p + k] = q.lm2;
-            inv[p + k] = q.inv_mkt;
+            double* r = flat + 12 * (p + (k >> 2)) + (k & 3);
+            r[0] = q.lm;
+            r[4] = q.lm2;
+            r[8] = q.inv_mkt;
         }
         if (threadIdx.x == 0) {
             p0[s] = p;
@@ -216,8 +221,9 @@ __device__ PGrid stage_pgrid(const SurfaceView& sv, unsigned char* smem) {
             d[ns + s] = sv.lnf_hi[s];
             d[2 * ns + s] = sv.lnf_lo[s];
         }
-        p += n4;
+        p += n4 >> 2;
     }
+    for (int k = threadIdx.x; k < 12 * (nqd - p); k += blockDim.x) flat[12 * p + k] = 0.0;
     __syncthreads();
     PGrid g;
     g.ns = ns;
@@ -226,9 +232,7 @@ __device__ PGrid stage_pgrid(const SurfaceView& sv, unsigned char* smem) {
     g.lnf_lo = d + 2 * ns;
     g.p0 = p0;
     g.nq = nq;
-    g.lm = lm;
-    g.lm2 = lm2;
-    g.inv = inv;
+    g.rec = rec;
     g.tab = nullptr;
     return g;
 }
@@ -245,41 +249,58 @@ __device__ __forceinline__ double quad_rel(const QuadTerms& t, double lm, double
     return fma(-fma(t.a2, lm2, fma(t.a1, lm, t.c0)), inv, 1.0);
 }
 
-// Sum of squared relative errors over slice s (calibration.cpp:253-267),
-// four partial sums by quote index mod 4 (see slice_cost).
-__device__ __forceinline__ double pslice_cost(const SmileTerms& st, const PGrid& g, int s) {
-    const QuadTerms t = quad_terms(st);
-    const int p0 = g.p0[s], n = g.nq[s];
-    const double2* lm = reinterpret_cast<const double2*>(g.lm + p0);
-    const double2* lm2 = reinterpret_cast<const double2*>(g.lm2 + p0);
-    const double2* inv = reinterpret_cast<const double2*>(g.inv + p0);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+// Sum of squared relative errors over one slice (calibration.cpp:253-267) for
+// C candidates at once: one set of quote loads feeds all C.  Four partial
+// sums per candidate by quote index mod 4: the dependency latency of a single
+// accumulator was the kernel's top stall; the reassociation moves the result
+// by ~1 ulp of the cost.  Each candidate's arithmetic and summation order do
+// not depend on C (the one- and two-chain kernels produce identical values).
+// The next quad's record is loaded while the current one is computed.
+template <int C>
+__device__ __forceinline__ void quad_cost_n(const QuadTerms (&t)[C], const QuadRec* __restrict__ r,
+                                            int n, double (&out)[C]) {
+    double acc[C][4];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0.0;
+    QuadRec cur = r[0];
     const int full = n >> 2;
-    int k = 0;
 #pragma unroll 1
-    for (; k < full; ++k) {
-        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
-        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
-        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
-        const double r0 = quad_rel(t, la.x, ma.x, ia.x), r1 = quad_rel(t, la.y, ma.y, ia.y);
-        const double r2 = quad_rel(t, lb.x, mb.x, ib.x), r3 = quad_rel(t, lb.y, mb.y, ib.y);
-        s0 = fma(r0, r0, s0);
-        s1 = fma(r1, r1, s1);
-        s2 = fma(r2, r2, s2);
-        s3 = fma(r3, r3, s3);
+    for (int k = 0; k < full; ++k) {
+        const QuadRec nxt = r[k + 1];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const double r0 = quad_rel(t[c], cur.lm01.x, cur.sq01.x, cur.inv01.x);
+            const double r1 = quad_rel(t[c], cur.lm01.y, cur.sq01.y, cur.inv01.y);
+            const double r2 = quad_rel(t[c], cur.lm23.x, cur.sq23.x, cur.inv23.x);
+            const double r3 = quad_rel(t[c], cur.lm23.y, cur.sq23.y, cur.inv23.y);
+            acc[c][0] = fma(r0, r0, acc[c][0]);
+            acc[c][1] = fma(r1, r1, acc[c][1]);
+            acc[c][2] = fma(r2, r2, acc[c][2]);
+            acc[c][3] = fma(r3, r3, acc[c][3]);
+        }
+        cur = nxt;
     }
     const int rem = n & 3;
     if (rem) {
-        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
-        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
-        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
-        const double r0 = quad_rel(t, la.x, ma.x, ia.x), r1 = quad_rel(t, la.y, ma.y, ia.y);
-        const double r2 = quad_rel(t, lb.x, mb.x, ib.x);
-        s0 = fma(r0, r0, s0);
-        if (rem > 1) s1 = fma(r1, r1, s1);
-        if (rem > 2) s2 = fma(r2, r2, s2);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const double r0 = quad_rel(t[c], cur.lm01.x, cur.sq01.x, cur.inv01.x);
+            const double r1 = quad_rel(t[c], cur.lm01.y, cur.sq01.y, cur.inv01.y);
+            const double r2 = quad_rel(t[c], cur.lm23.x, cur.sq23.x, cur.inv23.x);
+            acc[c][0] = fma(r0, r0, acc[c][0]);
+            if (rem > 1) acc[c][1] = fma(r1, r1, acc[c][1]);
+            if (rem > 2) acc[c][2] = fma(r2, r2, acc[c][2]);
+        }
     }
-    return (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[c] = (acc[c][0] + acc[c][1]) + (acc[c][2] + acc[c][3]);
+}
+
+__device__ __forceinline__ double pslice_cost(const SmileTerms& st, const PGrid& g, int s) {
+    const QuadTerms t[1] = {quad_terms(st)};
+    double out[1];
+    quad_cost_n<1>(t, g.rec + g.p0[s], g.nq[s], out);
+    return out[0];
 }
 
 __device__ __forceinline__ double static_cost(const double* v, const PGrid& g) {
@@ -303,64 +324,28 @@ __device__ __forceinline__ double case1_cost(const double* v, const PGrid& g) {
 }
 
 // ------------------------------------- C chains per thread (shared loads) ---
-// pslice_cost for C candidates at once: one set of quote loads feeds all C
-// (the per-candidate arithmetic and summation order are those of
-// pslice_cost, so each result is bit-identical to the single-chain path).
-template <int C>
-__device__ __forceinline__ void pslice_cost_n(const QuadTerms (&t)[C], const PGrid& g, int s,
-                                              double (&out)[C]) {
-    const int p0 = g.p0[s], n = g.nq[s];
-    const double2* lm = reinterpret_cast<const double2*>(g.lm + p0);
-    const double2* lm2 = reinterpret_cast<const double2*>(g.lm2 + p0);
-    const double2* inv = reinterpret_cast<const double2*>(g.inv + p0);
-    double acc[C][4];
-#pragma unroll
-    for (int c = 0; c < C; ++c) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0.0;
-    const int full = n >> 2;
-    int k = 0;
-#pragma unroll 1
-    for (; k < full; ++k) {
-        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
-        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
-        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const double r0 = quad_rel(t[c], la.x, ma.x, ia.x), r1 = quad_rel(t[c], la.y, ma.y, ia.y);
-            const double r2 = quad_rel(t[c], lb.x, mb.x, ib.x), r3 = quad_rel(t[c], lb.y, mb.y, ib.y);
-            acc[c][0] = fma(r0, r0, acc[c][0]);
-            acc[c][1] = fma(r1, r1, acc[c][1]);
-            acc[c][2] = fma(r2, r2, acc[c][2]);
-            acc[c][3] = fma(r3, r3, acc[c][3]);
-        }
-    }
-    const int rem = n & 3;
-    if (rem) {
-        const double2 la = lm[2 * k], lb = lm[2 * k + 1];
-        const double2 ma = lm2[2 * k], mb = lm2[2 * k + 1];
-        const double2 ia = inv[2 * k], ib = inv[2 * k + 1];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const double r0 = quad_rel(t[c], la.x, ma.x, ia.x), r1 = quad_rel(t[c], la.y, ma.y, ia.y);
-            const double r2 = quad_rel(t[c], lb.x, mb.x, ib.x);
-            acc[c][0] = fma(r0, r0, acc[c][0]);
-            if (rem > 1) acc[c][1] = fma(r1, r1, acc[c][1]);
-            if (rem > 2) acc[c][2] = fma(r2, r2, acc[c][2]);
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) out[c] = (acc[c][0] + acc[c][1]) + (acc[c][2] + acc[c][3]);
+// The single slice of a static objective, hoisted into registers for the
+// whole chain loop.
+struct StaticSlice {
+    double lnf_hi, lnf_lo, T;
+    const QuadRec* rec;
+    int nq;
+};
+
+__device__ __forceinline__ StaticSlice static_slice(const PGrid& g) {
+    return StaticSlice{g.lnf_hi[0], g.lnf_lo[0], g.T[0], g.rec + g.p0[0], g.nq[0]};
 }
 
-template <int C, int DIMF>
-__device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const PGrid& g,
-                                              double (&out)[C]) {
+template <int C, int DIMF, bool FAST>
+__device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const StaticSlice& sl,
+                                              const double2* tab, double (&out)[C]) {
     QuadTerms t[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
-        t[c] = quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, g.T[0]));
+        const double pw = pow_fwd<!FAST>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
+        t[c] = quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, sl.T));
     }
-    pslice_cost_n<C>(t, g, 0, out);
+    quad_cost_n<C>(t, sl.rec, sl.nq, out);
 }
 
 template <int C, int DIMF>
@@ -379,7 +364,7 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const P
             t[c] = quad_terms(dynamic_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T));
         }
         double s[C];
-        pslice_cost_n<C>(t, g, i, s);
+        quad_cost_n<C>(t, g.rec + g.p0[i], g.nq[i], s);
 #pragma unroll
         for (int c = 0; c < C; ++c) out[c] += s[c];
     }
@@ -588,8 +573,21 @@ __device__ __forceinline__ double propose_coord(double x, double step_scale, dou
     return (v < lo) ? lo : (hi < v) ? hi : v;
 }
 
+// propose_coord when the host has shown (sa_fast_path) that, for every
+// x in [lo, hi] and |step| <= range, one reflection lands inside the box:
+// then the reference's second reflection and its clamp never fire, and the
+// coordinate is one of {v, 2hi - v, 2lo - v} (two compares, no clamp).
+__device__ __forceinline__ double propose_coord_fast(double x, double step_scale, double lo, double hi,
+                                                     double lo2, double hi2, Xoshiro& rng) {
+    const double v = __dadd_rn(x, __dmul_rn(step_scale, rng.sym()));
+    const double rh = __dsub_rn(hi2, v), rl = __dsub_rn(lo2, v);
+    return (v > hi) ? rh : (v < lo) ? rl : v;
+}
+
 // One temperature level of this rank's chains (annealer.cpp:99-161).
-// ALLFREE: every coordinate is searched (no per-coordinate mask test).
+// ALLFREE (the FAST variant): every coordinate is searched (no mask test),
+// one reflection always lands in the box (propose_coord_fast) and every
+// forward has |ln f| <= 700 (unsaturated exp in pow_fwd) - see sa_fast_path.
 template <int KIND, int DIMF, bool ALLFREE, bool SMEM>
 __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
     sa_level_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
@@ -643,7 +641,9 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
             if (ev >= cap) break;  // annealer.cpp:120
 #pragma unroll
             for (int i = 0; i < DIMF; ++i) {
-                if (ALLFREE || ((a.free_mask >> i) & 1u))
+                if (ALLFREE)
+                    y[i] = propose_coord_fast(x[i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i], a.hi2[i], rng);
+                else if ((a.free_mask >> i) & 1u)
                     y[i] = propose_coord(x[i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i], a.hi2[i], rng);
                 else
                     y[i] = x[i];
@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
                 const double d = fy - fx;
                 const double q0 = d * inv_temp;
                 const double q = fma(fma(-q0, temp, d), inv_temp, q0);
-                accept = rng.uniform() < exp_tab(-q, tab_s);
+                const double u = rng.uniform();
+                accept = ALLFREE ? (q <= 700.0 && u < exp_tab_unsat(-q, tab_s)) : u < exp_tab(-q, tab_s);
             }
             if (accept) {
 #pragma unroll
@@ -755,12 +756,17 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
         double step_scale[DIMF];
 #pragma unroll
         for (int i = 0; i < DIMF; ++i) step_scale[i] = __dmul_rn(a.range[i], scale);
+        StaticSlice sl{};
+        if constexpr (KIND == OBJ_STATIC) sl = static_slice(g);
         for (int step = 0; step < steps; ++step) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
 #pragma unroll
                 for (int i = 0; i < DIMF; ++i) {
-                    if (ALLFREE || ((a.free_mask >> i) & 1u))
+                    if (ALLFREE)
+                        y[c][i] = propose_coord_fast(x[c][i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i],
+                                                     a.hi2[i], rng[c]);
+                    else if ((a.free_mask >> i) & 1u)
                         y[c][i] = propose_coord(x[c][i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i],
                                                 a.hi2[i], rng[c]);
                     else
@@ -768,27 +774,36 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
                 }
             }
             double fy[C];
-            if constexpr (KIND == OBJ_STATIC) static_cost_n<C, DIMF>(y, g, fy);
+            if constexpr (KIND == OBJ_STATIC) static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
             else case1_cost_n<C, DIMF>(y, g, fy);
+            // Metropolis (annealer.cpp:125-126) without a branch, so the
+            // chains' exp chains interleave: exp(-(fy - fx)/T) and the
+            // candidate uniform are computed for every chain; the uniform's
+            // draw is committed (the stream advanced) only when fy > fx, as
+            // the reference draws it.  (fy - fx) / T as in sa_level_kernel.
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (isnan(fy[c])) fy[c] = CUDART_INF;
-                bool accept = fy[c] <= fx[c];
-                if (!accept) {
-                    const double d = fy[c] - fx[c];
-                    const double q0 = d * inv_temp;
-                    const double q = fma(fma(-q0, temp, d), inv_temp, q0);
-                    accept = rng[c].uniform() < exp_tab(-q, tab_s);
-                }
-                if (accept) {
+                const bool up = !(fy[c] <= fx[c]);
+                const double d = fy[c] - fx[c];
+                const double q0 = d * inv_temp;
+                const double q = fma(fma(-q0, temp, d), inv_temp, q0);
+                const double u = rng[c].peek_uniform();
+                Xoshiro adv = rng[c];
+                adv.advance();
+                if (up) rng[c] = adv;
+                // exp_tab(-q) is 0 for q > 700 (and NaN for NaN q): u < 0 is
+                // false.  Non-short-circuit ops: no branch around the exp.
+                const double ex = ALLFREE ? exp_tab_unsat(-q, tab_s) : exp_tab(-q, tab_s);
+                const bool accept = ALLFREE ? (!up | ((q <= 700.0) & (u < ex))) : (!up | (u < ex));
+                const bool better = accept && fy[c] < bv[c];
 #pragma unroll
-                    for (int i = 0; i < DIMF; ++i) x[c][i] = y[c][i];
-                    fx[c] = fy[c];
-                    if (fx[c] < bv[c]) {
-                        bv[c] = fx[c];
+                for (int i = 0; i < DIMF; ++i) x[c][i] = accept ? y[c][i] : x[c][i];
+                fx[c] = accept ? fy[c] : fx[c];
+                bv[c] = better ? fy[c] : bv[c];
+                if (better) {
 #pragma unroll
-                        for (int i = 0; i < DIMF; ++i) bp_s[c][i][threadIdx.x] = x[c][i];
-                    }
+                    for (int i = 0; i < DIMF; ++i) bp_s[c][i][threadIdx.x] = y[c][i];
                 }
             }
         }
@@ -1109,7 +1124,8 @@ template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>((a.n_local + kLevelThreads - 1) / kLevelThreads);
-    const bool all_free = a.free_mask == (1u << DIMF) - 1u;
+    const bool all_free = a.fast != 0 && a.free_mask == (1u << DIMF) - 1u &&
+                          (KIND == OBJ_BUILTIN || sv.max_abs_lnf <= 700.0);
     const double inv_temp = 1.0 / temp;
     auto run = [&](auto k, size_t smem) {
         cudaError_t e = set_smem(k, smem);

@@ -1,7 +1,9 @@
-"""The two T_I level kernels (one chain per thread, and kCpt chains per thread
-sharing the quote loads; kernels_sa.cu) must produce bit-identical annealer
-trajectories.  The one-chain kernel is selected with SABR_SA_CPT=1, read once
-per process, so each variant runs in its own subprocess."""
+"""The T_I level kernel variants must produce bit-identical annealer
+trajectories: one chain per thread vs kCpt chains per thread sharing the quote
+loads (SABR_SA_CPT=1 selects the former), and the FAST propose/exp path
+(one reflection, unsaturated exp; kernels_sa.cu propose_coord_fast) vs the
+general one (SABR_SA_FAST=0).  The switches are read once per process, so
+each variant runs in its own subprocess."""
 import json
 import os
 import subprocess
@@ -40,11 +42,14 @@ print(json.dumps(out))
 """
 
 
-def run_variant(cpt):
+def run_variant(cpt, fast=None):
     env = dict(os.environ)
     env.pop("SABR_SA_CPT", None)
+    env.pop("SABR_SA_FAST", None)
     if cpt is not None:
         env["SABR_SA_CPT"] = str(cpt)
+    if fast is not None:
+        env["SABR_SA_FAST"] = str(fast)
     p = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
@@ -57,3 +62,10 @@ def test_multi_chain_kernel_matches_single_chain_kernel():
     assert multi.keys() == single.keys()
     for k in multi:
         assert multi[k] == single[k], k
+
+
+def test_fast_propose_matches_general_propose():
+    fast = run_variant(None)
+    general = run_variant(None, fast=0)
+    for k in fast:
+        assert fast[k] == general[k], k
