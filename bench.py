@@ -59,6 +59,37 @@ def c4_setup(levels=2):
     return surf, fixed, sch, plan
 
 
+# C5 (BASELINE.json configs[4]): full Case II MC calibration on the synthetic
+# 20-maturity x 30-strike surface (tests/data/synth20x30.csv, generated from
+# the published FX Case II fit by tests/golden/make_synth.py).  Search box:
+# the default Case II box narrowed to +-2% of its width around that fit (the
+# full box at T = t0 proposes exploding dynamics, which the reference aborts
+# on), every parameter free.
+CASE2_DEFAULTS = [("alpha", 1e-4, 2.0), ("beta", 0.0, 1.0), ("rho0", -1.0, 1.0), ("q_rho", -15.0, 15.0),
+                  ("d_rho", -1.0, 1.0), ("nu0", 1e-4, 10.0), ("q_nu", -15.0, 15.0), ("d_nu", -1.0, 1.0),
+                  ("a", 0.0, 150.0), ("b", 0.0, 150.0)]
+FX_CASE2 = [0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807, 0.0, 150.0]
+
+
+def c5_bounds(width=0.02):
+    out = {}
+    for (name, lo, hi), p in zip(CASE2_DEFAULTS, FX_CASE2):
+        h = width * (hi - lo)
+        out[name] = (max(lo, p - h), min(hi, p + h))
+    return out
+
+
+def c5_setup(chains=2048, num_paths=4096):
+    """C5 sample: one temperature level, one SA step of `chains` chains."""
+    import paper_2407_20713_b200 as pkg
+
+    surf = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "synth20x30.csv"))
+    sch = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=1, workers=chains // 8, groups=8, t_min=1.5,
+                                seed=1, max_evals=10 ** 12)
+    plan = pkg.SimulationPlan(num_paths=num_paths, dt=1 / 250, seed=1, rng="xoshiro")
+    return surf, c5_bounds(), sch, plan
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
 
@@ -302,6 +333,30 @@ def secondary(eng, torch, dev, stream):
             "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,
             "steps_per_path": steps_per_eval, "rng": plan.rng, "precision": precision, "seconds": secs,
             "final_cost": rep.final_cost, "mc_kernel_ms": t.kernel_ms, "mc_launches": t.kernel_launches}
+    # C5: full Case II MC calibration on the 20x30 synthetic surface, one SA step of 2048 chains
+    surf, bounds, sch, plan = c5_setup()
+    for precision in ("fp64", "fp32"):
+        plan.precision = precision
+        warm = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=1, workers=8, t_min=1.5, seed=1)
+        eng.calibrate_case2_T2(surf, bounds, warm, plan, None)
+        flush_l2(torch, dev)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        rep = eng.calibrate_case2_T2(surf, bounds, sch, plan, None)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = eng.last_timing()
+        secs = e0.elapsed_time(e1) / 1e3
+        steps = t.path_steps / max(1, plan.num_paths * (rep.evals - 1))  # sum of per-slice steps
+        out["c5_mc_calibration" + ("" if precision == "fp64" else "_fp32")] = {
+            "metric": f"MC SABR path-steps/s (calibrate_case2_T2, full Case II, C5 20x30 surface, {precision})",
+            "unit": "path-steps/s", "value": t.path_steps / secs,
+            "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
+            "cost_evals": rep.evals - 1, "levels": 1, "chains": sch.workers * sch.groups,
+            "paths": plan.num_paths, "steps_per_path_all_slices": steps, "rng": plan.rng,
+            "precision": precision, "seconds": secs, "final_cost": rep.final_cost,
+            "sample": "one SA step (L=1, one level) of 2048 chains; C5 names 1e6 chains over 8 GPUs "
+                      "(125000 per GPU, ~61x this sample per GPU-step)"}
     # C3: Case I joint calibration, EUR/USD, beta = 1 (acceptance.cpp:317-339 schedule, 1e5 chains)
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
     s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8, t_min=1e-7,

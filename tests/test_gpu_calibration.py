@@ -1,6 +1,8 @@
 """calibrate_* through the C-ABI against the compiled reference's own
 calibrate_* (proj/src/calibration.cpp) and its unit tests
 (proj/tests/test_calibration.cpp)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -99,6 +101,26 @@ def test_case2_T2_matches_reference(engine, ref, eq_surface):
     assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
     for k in r.params:
         assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
+    for a, b in zip(g.rows, r.rows):
+        assert abs(a.model - b.model) <= 1e-9 * abs(b.model)
+
+
+def test_case2_T2_full_case2_synthetic_surface(engine, ref):
+    """The C5 shape at small scale: every Case II parameter free (beta too),
+    the 20-maturity x 30-strike synthetic surface, reference xoshiro streams,
+    box narrowed around the published FX fit as in bench.py (c5_bounds)."""
+    import bench
+
+    surf = pkg.parse_surface(os.path.join(os.path.dirname(__file__), "data", "synth20x30.csv"))
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=4, t_min=0.9, seed=4)
+    plan = pkg.SimulationPlan(num_paths=256, seed=2)
+    g = engine.calibrate_case2_T2(surf, bench.c5_bounds(), s, plan, None)
+    r = ref.calibrate_case2_T2(surf, bench.c5_bounds(), s, plan, None)
+    assert g.evals == r.evals
+    assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
+    for k in r.params:
+        assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
+    assert len(g.rows) == len(r.rows) == 600
     for a, b in zip(g.rows, r.rows):
         assert abs(a.model - b.model) <= 1e-9 * abs(b.model)
 
