@@ -113,18 +113,24 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
                 }
                 box_muller(ua, ub, z1, z2);
             };
-            // all candidates' log-Euler step i with the shared normals
-            auto advance_all = [&](int i, const StepCoef* crow, double z1, double z2) {
-                const double h = __ldg(hdt + i);
+            // all candidates' log-Euler step with the shared normals; each
+            // candidate's coefficients of the NEXT step are loaded right after
+            // its current ones are used (rolling prefetch: the L1 latency of
+            // these uniform loads was the top stall, long_scoreboard)
+            double2 qa[CB], qb[CB];
+            auto load_row = [&](const StepCoef* row, int cc) {
+                qa[cc] = __ldg(reinterpret_cast<const double2*>(row + cc));
+                qb[cc] = __ldg(reinterpret_cast<const double2*>(row + cc) + 1);
+            };
+            auto advance_all = [&](double h, double z1, double z2, const StepCoef* next) {
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
-                    const double2 qa = __ldg(reinterpret_cast<const double2*>(crow + cc));
-                    const double2 qb = __ldg(reinterpret_cast<const double2*>(crow + cc) + 1);
                     const double arg = ((logn_mask >> cc) & 1u) ? la[cc] : fma(bm1[cc], lnf0 + x[cc], la[cc]);
                     const double nh = exp_tab(arg, tab);
-                    la[cc] += fma(qa.x, z1, -qa.y);
-                    const double u = fma(qb.y, z2, qb.x * z1);
+                    la[cc] += fma(qa[cc].x, z1, -qa[cc].y);
+                    const double u = fma(qb[cc].y, z2, qb[cc].x * z1);
                     x[cc] = fma(nh, fma(-nh, h, u), x[cc]);
+                    if (next != nullptr) load_row(next, cc);
                 }
             };
             // software pipeline: the (serial) Box-Muller chain of step i+1 is
@@ -132,18 +138,24 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
             // one basic block; the draw order is the reference's (2 per step)
             // and the last step is peeled so consecutive paths of a thread
             // continue the block stream exactly.
+            const StepCoef* crow = crow0;
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) load_row(crow, cc);
+            double h = __ldg(hdt);
             double z1, z2;
             normals(0, z1, z2);
-            const StepCoef* crow = crow0;
             const int n = sl.n_steps;
-            for (int i = 0; i + 1 < n; ++i, crow += cstride) {
+            for (int i = 0; i + 1 < n; ++i) {
                 double n1, n2;
                 normals(i + 1, n1, n2);
-                advance_all(i, crow, z1, z2);
+                const double hn = __ldg(hdt + i + 1);
+                crow += cstride;
+                advance_all(h, z1, z2, crow);
+                h = hn;
                 z1 = n1;
                 z2 = n2;
             }
-            advance_all(n - 1, crow, z1, z2);
+            advance_all(h, z1, z2, nullptr);
         }
         double F[CB];
 #pragma unroll

@@ -4,6 +4,7 @@
   python tools/profile_kernels.py case1   # C3 Case I level kernel (1e5 chains, 3 levels)
   python tools/profile_kernels.py t2      # C4 T_II: one level, 3 SA steps (MC tile kernel)
   python tools/profile_kernels.py mc      # price_european_batch, 2^20 paths (C4 pricing)
+  python tools/profile_kernels.py c5      # C5 T_II: full Case II, 20x30 surface, 512 chains, 1 step
 """
 import os
 import sys
@@ -37,6 +38,12 @@ def main(mode):
         plan = pkg.SimulationPlan(num_paths=1 << 20, seed=3, rng=os.environ.get("SABR_RNG", "xoshiro"))
         p = pkg.StaticSabrParams(0.375162, 0.999999, 0.331441, -0.999999)
         r = eng.price_european_batch(p, 2257.37, [2257.37], 0.018196, 0.034516, 0.495890, plan)
+    elif mode == "c5":
+        import bench
+
+        surf, bounds, s, plan = bench.c5_setup(chains=512)
+        plan.precision = os.environ.get("SABR_PRECISION", "fp64")
+        r = eng.calibrate_case2_T2(surf, bounds, s, plan, None)
     else:
         raise SystemExit(__doc__)
     print(mode, "evals" if hasattr(r, "evals") else "", getattr(r, "evals", r))
