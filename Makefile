@@ -11,7 +11,7 @@ OBJ_DIR  := build/obj
 LIB      := paper_2407_20713_b200/lib/libsabr_b200.so
 
 CU_SRCS  := $(SRC_DIR)/kernels_sa.cu $(SRC_DIR)/kernels_mc.cu $(SRC_DIR)/engine.cu \
-            $(SRC_DIR)/t2_driver.cu $(SRC_DIR)/peak.cu $(SRC_DIR)/kernels_c2f.cu
+            $(SRC_DIR)/t2_driver.cu $(SRC_DIR)/peak.cu $(SRC_DIR)/kernels_c2f.cu $(SRC_DIR)/kernels_bs.cu
 CPP_SRCS := $(SRC_DIR)/xoshiro_jump.cpp
 OBJS     := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(CU_SRCS)) \
             $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/%.o,$(CPP_SRCS))

@@ -264,7 +264,10 @@ SABR_API sabr_status sabr_cost_batch(sabr_ctx* ctx, int32_t model, const sabr_su
                                      const sabr_plan* plan, double* cost);
 
 /* Per-quote model vols for a batch of parameter vectors (static: the slice
- * only; case1: all quotes). vols[i*n_quotes + j].  analytics.cpp:183-205, :291-312 */
+ * only; case1 and case2: all quotes). vols[i*n_quotes + j].
+ * analytics.cpp:183-205, :291-312; case2 rows are 11 wide (horizon last) and
+ * use dyn_coeffs_case2 with its default 64 Gauss-Legendre nodes
+ * (analytics.hpp:25-26), as the smile command does (sabr_cli.cpp:234-243). */
 SABR_API sabr_status sabr_implied_vol_batch(sabr_ctx* ctx, int32_t model,
                                             const sabr_surface* surface, int64_t slice,
                                             const double* params, int64_t n, double* vols);
@@ -376,6 +379,22 @@ SABR_API sabr_status sabr_bench_fp64_peak(sabr_ctx* ctx, double* tflops);
 SABR_API sabr_status sabr_black_scholes_call(double spot, double strike, double rate,
                                              double dividend, double maturity, double vol,
                                              double* price);
+
+/* Batched black_scholes_call / implied_vol_from_price (black_scholes.hpp:7-14,
+ * black_scholes.cpp:20-69) on the device, one contract per element (SoA,
+ * caller-owned host arrays of length n).  The reference's scalar functions
+ * throw std::domain_error; here the first rejected element in index order
+ * returns SABR_E_DOMAIN with the reference's message (the outputs are then
+ * unspecified).  implied_vol keeps the reference's bracket + safeguarded
+ * Newton iteration (|BS(vol) - price| < 1e-10 or 200 steps). */
+SABR_API sabr_status sabr_black_scholes_call_batch(sabr_ctx* ctx, int64_t n, const double* spot,
+                                                   const double* strike, const double* rate,
+                                                   const double* dividend, const double* maturity,
+                                                   const double* vol, double* price);
+SABR_API sabr_status sabr_implied_vol_from_price_batch(sabr_ctx* ctx, int64_t n, const double* price,
+                                                       const double* spot, const double* strike,
+                                                       const double* rate, const double* dividend,
+                                                       const double* maturity, double* vol);
 
 #ifdef __cplusplus
 }

@@ -1075,6 +1075,39 @@ double orc_black_scholes_call(double spot, double strike, double r, double y, do
     return df_div * (0.5 * erfc(-d1 / ORC_SQRT2)) - df_k * (0.5 * erfc(-d2 / ORC_SQRT2));
 }
 
+/* implied_vol_from_price, black_scholes.cpp:37-69 (bounds checked by the caller's
+ * orc_implied_vol_status): doubling bracket, then <= 200 Newton steps on vega
+ * with the bisection fallback and the |diff| < 1e-10 exit. */
+static double orc_norm_pdf(double x) { return exp(-0.5 * x * x) / sqrt(2.0 * ORC_PI); }
+
+int orc_implied_vol_from_price(double price, double spot, double strike, double r, double y,
+                               double T, double* vol_out) {
+    if (spot <= 0 || strike <= 0 || T <= 0) return SABR_E_DOMAIN;
+    const double lower = orc_black_scholes_call(spot, strike, r, y, T, 0.0);
+    const double upper = spot * exp(-y * T);
+    if (price <= lower || price >= upper) return SABR_E_DOMAIN;
+    double lo = 0.0, hi = 1.0;
+    while (orc_black_scholes_call(spot, strike, r, y, T, hi) < price) hi *= 2.0;
+    double vol = 0.5 * (lo + hi);
+    for (int it = 0; it < 200; ++it) {
+        const double v = orc_black_scholes_call(spot, strike, r, y, T, vol);
+        const double diff = v - price;
+        if (fabs(diff) < 1e-10) break;
+        if (diff > 0)
+            hi = vol;
+        else
+            lo = vol;
+        const double sd = vol * sqrt(T);
+        const double d1 = (log(spot / strike) + (r - y + 0.5 * vol * vol) * T) / sd;
+        const double vega = spot * exp(-y * T) * orc_norm_pdf(d1) * sqrt(T);
+        double next = vol - diff / vega;
+        if (!(next > lo && next < hi)) next = 0.5 * (lo + hi);
+        vol = next;
+    }
+    *vol_out = vol;
+    return SABR_OK;
+}
+
 /* case2_mc_cost, calibration.cpp:399-416 with market_prices, :277-287 */
 int orc_cost_case2_mc(const sabr_surface* s, const double p[11], const sabr_plan* plan,
                       double* cost) {

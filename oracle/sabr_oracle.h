@@ -84,6 +84,8 @@ int orc_simulate_terminals(int model, const double* params, double forward0, dou
 int orc_price_european_batch(int model, const double* params, double spot,
                              const double* strikes, int64_t m, double rate, double dividend,
                              double T, const sabr_plan* plan, double* value, double* se);
+int orc_implied_vol_from_price(double price, double spot, double strike, double r, double y,
+                               double T, double* vol_out);
 double orc_black_scholes_call(double spot, double strike, double r, double y, double T,
                               double vol);
 /* price_cliquet, mc.cpp:275-320 */

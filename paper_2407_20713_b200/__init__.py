@@ -6,7 +6,7 @@ pricer, as hand-written sm_100a CUDA behind the C-ABI in include/sabr_b200.h.
 from ._abi import (LIB_PATH, MODEL_CASE1, MODEL_CASE2, MODEL_STATIC, RNG_PHILOX, RNG_XOSHIRO,
                    load_library)
 from .api import (AnnealingSchedule, AnnealResult, CalibrationReport, CaseIIParams, CaseIParams,
-                  ConstraintError, DomainError, Engine, NumericalError, OutOfRangeError,
+                  ConstraintError, DomainError, Engine, NumericalError, OutOfRangeError, ParseError,
                   PriceEstimate, ReportRow, SabrError, SimulationPlan, StaticSabrParams,
                   VolQuote, VolSlice, VolSurface, black_scholes_call, calibrate_case2_formula,
                   calibrate_case2_T2, calibrate_dynamic_case1_T1, calibrate_static_T1,

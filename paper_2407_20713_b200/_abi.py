@@ -189,7 +189,8 @@ EXPORTS = [
     "sabr_case2_feasible_batch", "sabr_mc_simulate_terminals",
     "sabr_mc_price_european_batch", "sabr_mc_price_cliquet", "sabr_minimize_builtin",
     "sabr_merge_level_records", "sabr_surface_csv_dims", "sabr_surface_csv_read",
-    "sabr_black_scholes_call", "sabr_bench_fp64_peak",
+    "sabr_black_scholes_call", "sabr_bench_fp64_peak", "sabr_black_scholes_call_batch",
+    "sabr_implied_vol_from_price_batch",
 ]
 
 _lib = None

@@ -51,6 +51,11 @@ class NumericalError(SabrError, RuntimeError):
     status = 4
 
 
+class ParseError(NumericalError):
+    """io::parse_error (io.hpp:14-24), a std::runtime_error: malformed surface
+    CSV or parameter file; the message carries "(line N)" when known."""
+
+
 class CudaError(SabrError, RuntimeError):
     status = 5
 
@@ -533,6 +538,8 @@ class Engine:
         n = P.shape[0] if P.ndim == 2 else 1
         nq = (len(surface.slices[slice].quotes) if model == A.MODEL_STATIC
               else surface.total_quotes())
+        if P.ndim == 2 and model == A.MODEL_CASE2 and P.shape[1] != 11:
+            raise ValueError("case2 parameter rows are 11 wide (horizon last)")
         out = np.empty((n, nq), dtype=np.float64)
         self._check(self.lib.sabr_implied_vol_batch(self._ctx, C.c_int32(model), C.byref(s),
                                                     C.c_int64(slice), _dptr(P), C.c_int64(n),
@@ -545,6 +552,23 @@ class Engine:
         self._check(self.lib.sabr_case2_feasible_batch(
             self._ctx, _dptr(P), C.c_int64(P.shape[0]), out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out.astype(bool)
+
+    # -- Black-Scholes (black_scholes.hpp), batched on the device --
+    def _bs_batch(self, fn, cols):
+        arrs = np.broadcast_arrays(*(np.asarray(c, dtype=np.float64) for c in cols))
+        arrs = [np.ascontiguousarray(a.ravel()) for a in arrs]
+        out = np.zeros(arrs[0].size)
+        self._check(fn(self._ctx, C.c_int64(out.size), *(_dptr(a) for a in arrs), _dptr(out)))
+        return out.reshape(np.broadcast(*cols).shape)
+
+    def black_scholes_call_batch(self, spot, strike, rate, dividend, maturity, vol) -> np.ndarray:
+        """black_scholes_call (black_scholes.cpp:20-35) element-wise; arguments broadcast."""
+        return self._bs_batch(self.lib.sabr_black_scholes_call_batch, (spot, strike, rate, dividend, maturity, vol))
+
+    def implied_vol_from_price_batch(self, price, spot, strike, rate, dividend, maturity) -> np.ndarray:
+        """implied_vol_from_price (black_scholes.cpp:37-69) element-wise; arguments broadcast."""
+        return self._bs_batch(self.lib.sabr_implied_vol_from_price_batch,
+                              (price, spot, strike, rate, dividend, maturity))
 
     # -- Monte Carlo (mc.hpp) --
     def simulate_terminals(self, params, forward0: float, alpha0: float, maturity: float,
@@ -626,13 +650,22 @@ def default_engine() -> Engine:
         return _default
 
 
+def _raise_parse(st: int, lib) -> None:
+    """io::parse_error is a std::runtime_error: SABR_E_RUNTIME from the surface
+    loader is a ParseError (a NumericalError subclass)."""
+    msg = lib.sabr_last_error().decode()
+    if st == 4:  # SABR_E_RUNTIME
+        raise ParseError(msg)
+    raise_for_status(st, msg)
+
+
 def parse_surface(path: str) -> VolSurface:
     """io::parse_surface (proj/src/io.cpp:151-161), implemented by the C++ host."""
     lib = A.load_library()
     ns, nq = C.c_int64(), C.c_int64()
     st = lib.sabr_surface_csv_dims(path.encode(), C.byref(ns), C.byref(nq))
     if st != A.SABR_OK:
-        raise_for_status(st, lib.sabr_last_error().decode())
+        _raise_parse(st, lib)
     T, r, y = (np.zeros(ns.value) for _ in range(3))
     off = np.zeros(ns.value + 1, dtype=np.int64)
     K, v = np.zeros(nq.value), np.zeros(nq.value)
@@ -640,7 +673,7 @@ def parse_surface(path: str) -> VolSurface:
     st = lib.sabr_surface_csv_read(path.encode(), C.byref(spot), _dptr(T), _dptr(r), _dptr(y),
                                    off.ctypes.data_as(C.POINTER(C.c_int64)), _dptr(K), _dptr(v))
     if st != A.SABR_OK:
-        raise_for_status(st, lib.sabr_last_error().decode())
+        _raise_parse(st, lib)
     return VolSurface.from_arrays(spot.value, T, r, y, off, K, v)
 
 

@@ -369,7 +369,7 @@ void gauss_legendre(int n, double* nodes, double* weights) {
 
 // Device view of the calibrate_case2_formula objective (calibration.cpp:483-520).
 C2fView make_c2f_view(sabr_ctx* ctx, const HostSurface& s, const std::vector<double>& market,
-                      double horizon) {
+                      double horizon, int gl_n = 8) {
     if (s.n() > static_cast<size_t>(kMaxC2fSlices))
         fail(SABR_E_DOMAIN, "calibrate_case2_formula: at most 64 slices on the device");
     std::vector<C2fSlice> sl(s.n());
@@ -390,7 +390,7 @@ C2fView make_c2f_view(sabr_ctx* ctx, const HostSurface& s, const std::vector<dou
     v.sl = upload(ctx, "c2f_slices", sl);
     v.q = upload(ctx, "c2f_quotes", q);
     v.horizon = horizon;
-    v.gl_n = 8;  // dyn_coeffs_case2(p, T, 8), calibration.cpp:506
+    v.gl_n = gl_n;  // dyn_coeffs_case2(p, T, 8), calibration.cpp:506 (64: the default, model vols)
     gauss_legendre(v.gl_n, v.gl_x, v.gl_w);
     v.exptab = exp_table_device(ctx);
     return v;
@@ -1398,8 +1398,21 @@ SABR_API sabr_status sabr_implied_vol_batch(sabr_ctx* ctx, int32_t model,
             const auto v = device_vols(ctx, OBJ_CASE1, sv, std::vector<double>(params, params + 6 * n), 6,
                                        static_cast<int64_t>(surface.total_quotes()));
             std::copy(v.begin(), v.end(), vols);
+        } else if (model == SABR_MODEL_CASE2) {
+            // dynamic_implied_vol(dyn_coeffs_case2(p, T, 64), ...): the smile of
+            // sabr_cli.cpp:234-243; p = n x 11 (horizon last), validated first
+            for (int64_t i = 0; i < n; ++i) validate_case2(params + 11 * i);
+            const C2fView v = make_c2f_view(ctx, surface, std::vector<double>(surface.total_quotes(), 1.0),
+                                            n > 0 ? params[10] : 1.0, 64);
+            auto* dp = upload(ctx, "c2v_params", std::vector<double>(params, params + 11 * n));
+            const int64_t nq = static_cast<int64_t>(surface.total_quotes());
+            auto* dv = static_cast<double*>(dev_buf(ctx, "c2v_vols", sizeof(double) * std::max<int64_t>(1, n * nq)));
+            check_cuda(launch_c2f_vols(v, dp, n, dv, ctx->stream), "c2f_vols");
+            check_cuda(cudaMemcpyAsync(vols, dv, sizeof(double) * n * nq, cudaMemcpyDeviceToHost, ctx->stream),
+                       "D2H vols");
+            sync(ctx);
         } else {
-            fail(SABR_E_DOMAIN, "implied vols exist for the static and case1 models");
+            fail(SABR_E_DOMAIN, "unknown model");
         }
     });
 }
@@ -1689,6 +1702,65 @@ SABR_API sabr_status sabr_black_scholes_call(double spot, double strike, double 
     return guarded([&] {
         if (!price) fail(SABR_E_INVALID, "price is null");
         *price = black_scholes_call(spot, strike, rate, dividend, maturity, vol);
+    });
+}
+
+}
+
+namespace {
+// Upload the SoA inputs, run one batched Black-Scholes kernel, map the first
+// rejected element (index order) to the reference's domain_error message.
+template <class Launch>
+void bs_batch(sabr_ctx* ctx, int64_t n, std::initializer_list<const double*> in, double* out, Launch&& launch) {
+    std::vector<const double*> dev;
+    int k = 0;
+    for (const double* p : in) {
+        if (!p) fail(SABR_E_INVALID, "input array is null");
+        dev.push_back(upload(ctx, "bs_in" + std::to_string(k++), std::vector<double>(p, p + n)));
+    }
+    if (!out) fail(SABR_E_INVALID, "output array is null");
+    auto* dout = static_cast<double*>(dev_buf(ctx, "bs_out", sizeof(double) * n));
+    auto* dst = static_cast<int32_t*>(dev_buf(ctx, "bs_status", sizeof(int32_t) * n));
+    check_cuda(launch(dev, dout, dst), "black_scholes batch");
+    std::vector<int32_t> st(n);
+    check_cuda(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    check_cuda(cudaMemcpyAsync(st.data(), dst, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync(ctx);
+    for (int64_t i = 0; i < n; ++i) {
+        if (st[i] == BS_E_INPUTS) fail(SABR_E_DOMAIN, "black_scholes_call: spot, strike, maturity must be positive");
+        if (st[i] == BS_E_VOL) fail(SABR_E_DOMAIN, "black_scholes_call: vol must be nonnegative");
+        if (st[i] == BS_E_BOUNDS) fail(SABR_E_DOMAIN, "implied_vol_from_price: price outside no-arbitrage bounds");
+    }
+}
+}  // namespace
+
+extern "C" {
+
+SABR_API sabr_status sabr_black_scholes_call_batch(sabr_ctx* ctx, int64_t n, const double* spot,
+                                                   const double* strike, const double* rate,
+                                                   const double* dividend, const double* maturity,
+                                                   const double* vol, double* price) {
+    return guarded([&] {
+        CtxLock l(ctx);
+        if (n <= 0) return;
+        bs_batch(ctx, n, {spot, strike, rate, dividend, maturity, vol}, price,
+                 [&](const std::vector<const double*>& d, double* o, int32_t* st) {
+                     return launch_bs_call(n, d[0], d[1], d[2], d[3], d[4], d[5], o, st, ctx->stream);
+                 });
+    });
+}
+
+SABR_API sabr_status sabr_implied_vol_from_price_batch(sabr_ctx* ctx, int64_t n, const double* price,
+                                                       const double* spot, const double* strike,
+                                                       const double* rate, const double* dividend,
+                                                       const double* maturity, double* vol) {
+    return guarded([&] {
+        CtxLock l(ctx);
+        if (n <= 0) return;
+        bs_batch(ctx, n, {price, spot, strike, rate, dividend, maturity}, vol,
+                 [&](const std::vector<const double*>& d, double* o, int32_t* st) {
+                     return launch_implied_vol(n, d[0], d[1], d[2], d[3], d[4], d[5], o, st, ctx->stream);
+                 });
     });
 }
 

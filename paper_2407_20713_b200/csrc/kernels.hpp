@@ -121,4 +121,17 @@ cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double*
 cudaError_t launch_t2_level_end(const T2Chain* chains, const SaLevelArgs& a, int64_t level,
                                 cudaStream_t s);
 
+// ---- batched Black-Scholes (black_scholes.cpp:20-69), kernels_bs.cu ----
+enum BsStatus : int32_t {
+    BS_OK = 0,
+    BS_E_INPUTS = 1,  // "black_scholes_call: spot, strike, maturity must be positive"
+    BS_E_VOL = 2,     // "black_scholes_call: vol must be nonnegative"
+    BS_E_BOUNDS = 3,  // "implied_vol_from_price: price outside no-arbitrage bounds"
+};
+cudaError_t launch_bs_call(int64_t n, const double* spot, const double* strike, const double* r, const double* y,
+                           const double* T, const double* vol, double* out, int32_t* status, cudaStream_t s);
+cudaError_t launch_implied_vol(int64_t n, const double* price, const double* spot, const double* strike,
+                               const double* r, const double* y, const double* T, double* out, int32_t* status,
+                               cudaStream_t s);
+
 }  // namespace sabr_gpu

@@ -245,9 +245,10 @@ __device__ bool cta_feasible(const double* p, Shared& sh) {
     return cta_all(ok, sh);
 }
 
-// The calibrate_case2_formula objective (calibration.cpp:497-520) for the
-// full vector p (horizon last); every thread returns the same value.
-__device__ double c2f_objective(const double* p, const C2fView& v, Shared& sh) {
+// dyn_coeffs_case2 (analytics.cpp:219-289) for every slice and the
+// strike-independent Eq. 8 terms of dynamic_implied_vol (analytics.cpp:291-312)
+// into sh.terms[s], for the full vector p (horizon last).
+__device__ void c2f_slice_terms(const double* p, const C2fView& v, Shared& sh) {
     const Pieces c = make_pieces(p);
     const double2* tab = sh.tab;
     // exact nu1^2, nu2^2, eta1 per slice: one thread per slice
@@ -293,6 +294,12 @@ __device__ double c2f_objective(const double* p, const C2fView& v, Shared& sh) {
                                     pw, v.sl[s].T);
     }
     __syncthreads();
+}
+
+// The calibrate_case2_formula objective (calibration.cpp:497-520) for the
+// full vector p (horizon last); every thread returns the same value.
+__device__ double c2f_objective(const double* p, const C2fView& v, Shared& sh) {
+    c2f_slice_terms(p, v, sh);
     // quotes: vol -> BS price -> squared relative price error (calibration.cpp:507-517)
     bool ok = true;
     double sum = 0.0;
@@ -427,7 +434,29 @@ __global__ void __launch_bounds__(kT) c2f_cost_kernel(const __grid_constant__ C2
     if (threadIdx.x == 0) cost[blockIdx.x] = f;
 }
 
+// Case II model vols of every quote, one CTA per vector (validated on the host)
+__global__ void __launch_bounds__(kT) c2f_vol_kernel(const __grid_constant__ C2fView v,
+                                                     const double* __restrict__ params,
+                                                     double* __restrict__ vols) {
+    __shared__ Shared sh;
+    stage_tab(v, sh);
+    double p[11];
+    for (int i = 0; i < 11; ++i) p[i] = params[blockIdx.x * 11 + i];
+    c2f_slice_terms(p, v, sh);
+    for (int j = threadIdx.x; j < v.nq; j += kT) {
+        const C2fQuote q = v.q[j];
+        vols[static_cast<int64_t>(blockIdx.x) * v.nq + j] = smile_vol(sh.terms[q.slice], q.lm, q.lm2);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_c2f_vols(const C2fView& v, const double* params, int64_t n, double* vols,
+                            cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    c2f_vol_kernel<<<static_cast<unsigned>(n), kT, 0, s>>>(v, params, vols);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_c2f_level(const C2fView& v, const SaLevelArgs& a, int64_t level, double temp,
                              cudaStream_t s) {

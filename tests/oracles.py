@@ -363,6 +363,12 @@ class Restate:
     def black_scholes_call(self, spot, K, r, y, T, vol):
         return self.lib.orc_black_scholes_call(*(C.c_double(x) for x in (spot, K, r, y, T, vol)))
 
+    def implied_vol_from_price(self, price, spot, K, r, y, T):
+        out = C.c_double()
+        self._check(self.lib.orc_implied_vol_from_price(*(C.c_double(x) for x in (price, spot, K, r, y, T)),
+                                                        C.byref(out)))
+        return out.value
+
 
 def ref_parse_surface(path):
     """io::parse_surface through the compiled reference."""

@@ -162,3 +162,33 @@ def test_case2_formula_cost_parity(engine, ref, request, fixture):
     rel = np.abs(got[ok] - want[ok]) / np.maximum(np.abs(want[ok]), 1e-8)
     print(f"case2 formula {fixture}: {ok.sum()} finite, max rel {rel.max():.2e}")
     assert rel.max() < 1e-10
+
+
+def test_case2_model_vols_match_reference(engine, ref):
+    """Case II model vols dynamic_implied_vol(dyn_coeffs_case2(p, T, 64), ...)
+    (the smile command, sabr_cli.cpp:234-243) on the 20x30 synthetic surface,
+    which the reference generated from exactly these vols at the FX fit."""
+    import os
+
+    surface = pkg.parse_surface(os.path.join(os.path.dirname(__file__), "data", "synth20x30.csv"))
+    H = surface.slices[-1].maturity
+    fx_fit = [0.154037, 1.0, -0.693682, 0.345973, -0.200342, 7.541424, -0.992551, 0.339807, 0.0, 150.0, H]
+    P = np.vstack([fx_fit, feasible_case2_vectors(ref, 40, 8, H)])
+    got = engine.implied_vol_batch(pkg.MODEL_CASE2, surface, P)
+    worst = 0.0
+    for i, p in enumerate(P):
+        off = 0
+        for s, sl in enumerate(surface.slices):
+            c = ref.dyn_coeffs_case2(p, sl.maturity, 64)
+            f = surface.forward(s)
+            for j, q in enumerate(sl.quotes):
+                want = ref.dynamic_vol(c, p[0], p[1], q.strike, f, sl.maturity)
+                if np.isfinite(want) and want > 0:
+                    worst = max(worst, abs(got[i, off + j] - want) / abs(want))
+            off += len(sl.quotes)
+    # eta2^2 is a nested 64x64-node quadrature summed in another order (CTA
+    # reduction): measured worst 1.4e-12 relative over 41 vectors x 600 quotes
+    assert worst < 1e-11, worst
+    # the fixture's own vols (written as 100*vol in shortest form) at the fit
+    market = np.array([q.vol for sl in surface.slices for q in sl.quotes])
+    assert np.max(np.abs(got[0] - market) / market) < 1e-14

@@ -151,8 +151,34 @@ def test_black_scholes_matches_reference_fixture(orc):
     assert abs(p - 134.605) <= 2e-5 * 134.605
 
 
+def bs_contracts(n, seed=9):
+    """test_black_scholes.cpp:10-23 style random contracts (spot, K, r, y, T, vol)."""
+    rng = np.random.default_rng(seed)
+    spot = 50.0 + 4000.0 * rng.uniform(size=n)
+    return (spot, spot * (0.7 + 0.6 * rng.uniform(size=n)), 0.05 * rng.uniform(size=n),
+            0.05 * rng.uniform(size=n), 0.1 + 2.0 * rng.uniform(size=n), 0.05 + 0.5 * rng.uniform(size=n))
+
+
+def test_implied_vol_round_trip(orc):
+    # test_black_scholes.cpp:10-23: price -> implied vol recovers vol to 1e-8
+    # (for prices the 1e-10 price tolerance resolves: not the ~1e-18 deep OTM ones)
+    for c in zip(*bs_contracts(50)):
+        price = orc.black_scholes_call(*c)
+        if price > 1e-8 * c[0]:
+            assert abs(orc.implied_vol_from_price(price, *c[:5]) - c[5]) < 1e-8
+    with pytest.raises(ValueError):  # outside the no-arbitrage bounds (test_black_scholes.cpp:66-69)
+        orc.implied_vol_from_price(200.0, 100, 100, 0, 0, 1)
+
+
 @pytest.mark.skipif(not have_ref(), reason="oracle/_ref not built")
 class TestAgainstLiveReference:
+    def test_black_scholes_and_implied_vol(self, orc):
+        ref = Ref()
+        for c in zip(*bs_contracts(300, seed=4)):
+            p = orc.black_scholes_call(*c)
+            assert p == ref.black_scholes_call(*c)
+            assert orc.implied_vol_from_price(p, *c[:5]) == ref.implied_vol_from_price(p, *c[:5])
+
     def test_costs(self, orc):
         ref = Ref()
         eq = golden_surface("eurostoxx50")
