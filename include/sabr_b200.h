@@ -203,6 +203,16 @@ SABR_API sabr_status sabr_comm_unique_id(uint8_t out[128]);
 SABR_API sabr_status sabr_ctx_init_comm(sabr_ctx* ctx, const uint8_t uid[128],
                                         int32_t rank, int32_t nranks);
 
+/* The same rank decomposition with the per-level record exchange done by the
+ * caller on the host instead of NCCL (a non-NCCL transport, or several ranks
+ * sharing one GPU in tests).  Once per temperature level the engine calls
+ * fn(user, send, recv, bytes): send = this rank's `bytes`, recv = nranks *
+ * `bytes` in rank order (an all-gather), both host memory; fn returns 0 on
+ * success.  Results are identical to the NCCL path and to a single rank. */
+typedef int (*sabr_allgather_fn)(void* user, const void* send, void* recv, int64_t bytes);
+SABR_API sabr_status sabr_ctx_init_host_exchange(sabr_ctx* ctx, int32_t rank, int32_t nranks,
+                                                 sabr_allgather_fn fn, void* user);
+
 /* ---- calibration (proj/include/sabr/calibration.hpp) -------------------- */
 
 /* calibrate_static_T1, calibration.hpp:82-85 / proj/src/calibration.cpp:289-323 */

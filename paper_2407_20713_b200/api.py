@@ -435,6 +435,24 @@ class Engine:
         self.rank, self.nranks = rank, nranks
 
     # -- calibration (calibration.hpp:82-124) --
+    def init_host_exchange(self, rank: int, nranks: int, allgather) -> None:
+        """Split the chains over `nranks` ranks with the per-level record
+        exchange done on the host: allgather(send: bytes) -> bytes (nranks
+        records in rank order), e.g. over a torch.distributed gloo group."""
+        def cb(user, send, recv, nbytes):
+            try:
+                out = allgather(C.string_at(send, nbytes))
+                if len(out) != nbytes * nranks:
+                    return 1
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the engine as a failed exchange
+                return 1
+
+        self._exchange_cb = A.ALLGATHER_FN(cb)  # keep the trampoline alive
+        self._check(self.lib.sabr_ctx_init_host_exchange(self._ctx, C.c_int32(rank), C.c_int32(nranks),
+                                                         self._exchange_cb, None))
+
     def calibrate_static_T1(self, surface: VolSurface, slice: int, bounds=None,
                             schedule: Optional[AnnealingSchedule] = None, fixed=None,
                             trace: bool = False) -> CalibrationReport:

@@ -699,6 +699,16 @@ void allgather(sabr_ctx* ctx, const void* send, void* recv, size_t bytes) {
             check_cuda(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
         return;
     }
+    if (ctx->exchange) {  // host transport: D2H, caller's all-gather, H2D
+        std::vector<unsigned char> hs(bytes), hr(bytes * static_cast<size_t>(ctx->nranks));
+        check_cuda(cudaMemcpyAsync(hs.data(), send, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H record");
+        check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+        if (ctx->exchange(ctx->exchange_user, hs.data(), hr.data(), static_cast<int64_t>(bytes)) != 0)
+            fail(SABR_E_NCCL, "host exchange: the all-gather callback failed");
+        check_cuda(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, ctx->stream), "H2D records");
+        check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+        return;
+    }
     nccl_check(nccl().allGather(send, recv, bytes, ncclChar, static_cast<ncclComm_t>(ctx->comm),
                                 ctx->stream),
                "ncclAllGather");
@@ -1019,6 +1029,19 @@ SABR_API sabr_status sabr_comm_unique_id(uint8_t out[128]) {
         ncclUniqueId id;
         nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
         std::memcpy(out, id.internal, 128);
+    });
+}
+
+SABR_API sabr_status sabr_ctx_init_host_exchange(sabr_ctx* ctx, int32_t rank, int32_t nranks,
+                                                 sabr_allgather_fn fn, void* user) {
+    return guarded([&] {
+        CtxLock l(ctx);
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(SABR_E_INVALID, "bad rank/nranks");
+        if (nranks > 1 && !fn) fail(SABR_E_INVALID, "exchange callback is null");
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        ctx->exchange = nranks > 1 ? fn : nullptr;
+        ctx->exchange_user = user;
     });
 }
 

@@ -24,6 +24,9 @@ struct sabr_ctx {
     // NCCL (one communicator per context; chains are split over ranks)
     void* comm = nullptr;
     int rank = 0, nranks = 1;
+    // host-side record exchange instead of NCCL (sabr_ctx_init_host_exchange)
+    sabr_allgather_fn exchange = nullptr;
+    void* exchange_user = nullptr;
     // grow-only device scratch, keyed by purpose
     std::map<std::string, std::pair<void*, size_t>> bufs;
     // host cache of xoshiro jump tables keyed by (draws per entry, count)
