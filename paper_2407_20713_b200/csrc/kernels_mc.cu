@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
     int64_t idx = blockIdx.x;
-    const int tile = static_cast<int>(idx % P.n_tiles);
-    idx /= P.n_tiles;
+    const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
+    idx /= P.tile_count;
     const int s = static_cast<int>(idx % P.n_slices);
     const int g = static_cast<int>(idx / P.n_slices);
     const McSlice sl = P.slices[s];
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
             s2 += acc[((w * CB + cc) * mq + j) * 2 + 1];
         }
         double* out = P.partials +
-                      ((static_cast<int64_t>(c0 + cc) * P.n_quotes + sl.q_begin + j) * P.n_tiles + tile) * 2;
+                      ((static_cast<int64_t>(tile) * P.n_cand + c0 + cc) * P.n_quotes + sl.q_begin + j) * 2;
         out[0] = s1;
         out[1] = s2;
     }
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
     int64_t idx = blockIdx.x;
-    const int tile = static_cast<int>(idx % P.n_tiles);
-    idx /= P.n_tiles;
+    const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
+    idx /= P.tile_count;
     const int s = static_cast<int>(idx % P.n_slices);
     const int g = static_cast<int>(idx / P.n_slices);
     const McSlice sl = P.slices[s];
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
             s2 += acc[((w * CB + cc) * mq + j) * 2 + 1];
         }
         double* out = P.partials +
-                      ((static_cast<int64_t>(c0 + cc) * P.n_quotes + sl.q_begin + j) * P.n_tiles + tile) * 2;
+                      ((static_cast<int64_t>(tile) * P.n_cand + c0 + cc) * P.n_quotes + sl.q_begin + j) * 2;
         out[0] = s1;
         out[1] = s2;
     }
@@ -460,11 +460,13 @@ __global__ void mc_reduce_kernel(const McParams P, double* __restrict__ value,
     if (t >= static_cast<int64_t>(P.n_cand) * P.n_quotes) return;
     const int c = static_cast<int>(t / P.n_quotes);
     if (P.active != nullptr && P.active[c] == 0) return;
-    const double* p = P.partials + t * P.n_tiles * 2;
+    // tiles in fixed order (tile-major partials: coalesced over (c, q))
+    const int64_t stride = static_cast<int64_t>(P.n_cand) * P.n_quotes * 2;
+    const double* p = P.partials + t * 2;
     double s1 = 0.0, s2 = 0.0;
     for (int k = 0; k < P.n_tiles; ++k) {
-        s1 += p[2 * k];
-        s2 += p[2 * k + 1];
+        s1 += p[k * stride];
+        s2 += p[k * stride + 1];
     }
     const double n = static_cast<double>(P.num_paths);
     const double mean = s1 / n;
@@ -498,10 +500,15 @@ cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    const int n_groups = (p.n_cand + CB - 1) / CB;
-    const int64_t blocks = static_cast<int64_t>(p.n_tiles) * p.n_slices * n_groups;
+    McParams q = p;
+    if (q.tile_count <= 0) {
+        q.tile_begin = 0;
+        q.tile_count = q.n_tiles;
+    }
+    const int n_groups = (q.n_cand + CB - 1) / CB;
+    const int64_t blocks = static_cast<int64_t>(q.tile_count) * q.n_slices * n_groups;
     if (blocks <= 0) return cudaSuccess;
-    k<<<static_cast<unsigned>(blocks), kMcThreads, smem, s>>>(p);
+    k<<<static_cast<unsigned>(blocks), kMcThreads, smem, s>>>(q);
     return cudaGetLastError();
 }
 

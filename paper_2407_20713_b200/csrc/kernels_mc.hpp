@@ -32,6 +32,8 @@ struct McParams {
     int32_t n_quotes;       // total strikes over slices
     int32_t max_q;          // largest strike count of one slice
     int32_t n_tiles;        // path tiles per (candidate, slice)
+    int32_t tile_begin;     // this launch simulates tiles [tile_begin, tile_begin + tile_count)
+    int32_t tile_count;     // (<= 0: all n_tiles); T_II path sharding over ranks
     int32_t ppt;            // paths per thread (consecutive, same RNG block)
     int32_t rng;            // sabr_rng
     int64_t total_steps;    // row length of coef / hdt
@@ -48,7 +50,8 @@ struct McParams {
     const double* hdt;      // [total_steps] dt/2
     const double* strikes;  // [n_quotes]
     const uint64_t* jump;   // xoshiro jump polynomials, 4 words each
-    double* partials;       // [n_cand][n_quotes][n_tiles][2] (sum, sum of squares) or null
+    double* partials;       // [n_tiles][n_cand][n_quotes][2] (sum, sum of squares; tile-major so a
+                            // rank's tile range is one contiguous slab) or null
     double* terminals;      // [num_paths] (n_cand == 1, n_slices == 1) or null
     int* bad;               // [n_cand] non-finite flag
     const double2* exptab;  // [128] 2^(i/128) double-double (exp_tab, device_common.cuh)

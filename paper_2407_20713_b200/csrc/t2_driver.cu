@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "engine.hpp"
 
@@ -24,8 +26,19 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     const std::vector<double> temps = temperatures(sch);
     const int64_t L = static_cast<int64_t>(temps.size());
     const int64_t n_chains = static_cast<int64_t>(sch.workers) * sch.groups;
-    const int64_t begin = ctx->rank * n_chains / ctx->nranks;
-    const int64_t end = (ctx->rank + 1) * n_chains / ctx->nranks;
+    // Multi-rank decomposition.  Chains are split over the ranks
+    // (one record all-gather per level) unless there are fewer chains than
+    // ranks: then every rank runs every chain on its own slab of path tiles,
+    // and the tile partials of every MC step are all-gathered and reduced in
+    // the single-rank tile order, so costs, decisions and reports are the
+    // same on every rank and for any rank count.  SABR_T2_SHARD=paths forces
+    // the path split (tests).
+    const bool path_mode = ctx->nranks > 1 && (n_chains < ctx->nranks || [] {
+        const char* e = std::getenv("SABR_T2_SHARD");
+        return e != nullptr && std::string(e) == "paths";
+    }());
+    const int64_t begin = path_mode ? 0 : ctx->rank * n_chains / ctx->nranks;
+    const int64_t end = path_mode ? n_chains : (ctx->rank + 1) * n_chains / ctx->nranks;
     const int32_t n_local = static_cast<int32_t>(end - begin);
     const size_t ns = surface.n();
     const int nq = static_cast<int>(surface.total_quotes());
@@ -69,8 +82,14 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     const int64_t S = job.total_steps;
     const int32_t n_tiles = static_cast<int32_t>(
         (plan.num_paths + static_cast<uint64_t>(kMcThreads) * ppt - 1) / (static_cast<uint64_t>(kMcThreads) * ppt));
+    // path mode: rank r simulates tiles [r*tpr, min((r+1)*tpr, n_tiles)); the
+    // partial buffer holds nranks*tpr tiles (rank slabs in rank order)
+    const int32_t tpr = path_mode ? (n_tiles + ctx->nranks - 1) / ctx->nranks : n_tiles;
+    const int32_t tile_begin = path_mode ? ctx->rank * tpr : 0;
+    const int32_t tile_count = path_mode ? std::max(0, std::min(tpr, n_tiles - tile_begin)) : n_tiles;
+    const int64_t tiles_alloc = path_mode ? static_cast<int64_t>(tpr) * ctx->nranks : n_tiles;
     // candidates per MC launch: bound the coefficient and partial buffers
-    const int64_t per_cand = S * 32 + static_cast<int64_t>(nq) * n_tiles * 16;
+    const int64_t per_cand = S * 32 + static_cast<int64_t>(nq) * tiles_alloc * 16;
     const int32_t chunk = static_cast<int32_t>(
         std::max<int64_t>(1, std::min<int64_t>(std::max(n_local, 1), (int64_t(1) << 31) / std::max<int64_t>(per_cand, 1))));
     const bool fp32 = plan.precision == SABR_FP32;
@@ -113,7 +132,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     auto* nonfinite = static_cast<int*>(dev_buf(ctx, "t2_nonfinite", sizeof(int)));
     void* coef = dev_buf(ctx, "t2_coef", (fp32 ? sizeof(float4) : sizeof(StepCoef)) * S * stride);
     auto* partials = static_cast<double*>(
-        dev_buf(ctx, "t2_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * n_tiles * chunk));
+        dev_buf(ctx, "t2_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * tiles_alloc * chunk));
     auto* values = static_cast<double*>(dev_buf(ctx, "t2_values", sizeof(double) * static_cast<size_t>(nq) * chunk));
     check_cuda(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx->stream), "memset");
     check_cuda(cudaMemsetAsync(bad, 0, sizeof(int) * nl, ctx->stream), "memset");
@@ -128,7 +147,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
 
     SaLevelArgs a{};
     a.dim_full = 10;
-    a.nranks = ctx->nranks;
+    a.nranks = path_mode ? 1 : ctx->nranks;  // path mode: every rank holds every chain
     a.chain_begin = begin;
     a.n_local = n_local;
     a.n_chains = n_chains;
@@ -184,9 +203,15 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
                 Q.partials = partials;
                 Q.terminals = nullptr;
                 Q.bad = bad + c0;
+                Q.tile_begin = tile_begin;
+                Q.tile_count = tile_count;
                 timer.before();
-                check_cuda(launch_mc_tiles(Q, cb, ctx->stream), "mc_tiles");
+                if (tile_count > 0) check_cuda(launch_mc_tiles(Q, cb, ctx->stream), "mc_tiles");
                 timer.after();
+                if (path_mode) {  // in-place all-gather of the rank slabs [tpr tiles][nc][nq][2]
+                    const size_t slab = sizeof(double) * 2 * static_cast<size_t>(tpr) * nc * nq;
+                    allgather(ctx, reinterpret_cast<unsigned char*>(partials) + ctx->rank * slab, partials, slab);
+                }
                 check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, cost + c0, ctx->stream), "mc_reduce");
                 mc_launches += 1;
                 launches += 4;
@@ -195,7 +220,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
             launches += 2;
         }
         check_cuda(launch_t2_level_end(chains, a, level, ctx->stream), "t2_level_end");
-        if (ctx->nranks > 1) {
+        if (a.nranks > 1) {
             allgather(ctx, a.rank_rec, recv, sizeof(sabr_level_record));
             check_cuda(launch_sa_merge(a, recv, level, ctx->stream), "sa_merge");
         }
@@ -207,8 +232,19 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     sabr_sa_state out{};
     int nf = 0;
     check_cuda(cudaMemcpyAsync(&out, a.state, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
-    check_cuda(cudaMemcpyAsync(&nf, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    if (path_mode) {  // a non-finite path may sit in any rank's tiles: OR the flags
+        auto* flags = static_cast<int*>(dev_buf(ctx, "t2_nonfinite_all", sizeof(int) * ctx->nranks));
+        allgather(ctx, nonfinite, flags, sizeof(int));
+        std::vector<int> h(ctx->nranks);
+        check_cuda(cudaMemcpyAsync(h.data(), flags, sizeof(int) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+        for (int v : h) nf |= v;
+    }
+    int nf_local = 0;
+    check_cuda(cudaMemcpyAsync(&nf_local, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     check_cuda(cudaStreamSynchronize(ctx->stream), "sync");
+    nf |= nf_local;
     const double evals_run = static_cast<double>(out.evals - 1);
     timer.stop(evals_run, evals_run * static_cast<double>(plan.num_paths) * static_cast<double>(S),
                mc_launches, launches);

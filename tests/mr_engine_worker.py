@@ -40,6 +40,15 @@ def workloads(eng):
     s2 = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=3, workers=5, groups=2, t_min=0.2, seed=3)
     out["case2_T2"] = report_key(eng.calibrate_case2_T2(surf, None, s2, pkg.SimulationPlan(num_paths=4096, seed=1),
                                                         fixed, trace=True))
+    # fewer chains than ranks (1 chain): path tiles split over the ranks, partials all-gathered per step
+    s4 = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=4, workers=1, groups=1, t_min=0.2, seed=4)
+    out["case2_T2_one_chain"] = report_key(eng.calibrate_case2_T2(surf, None, s4, pkg.SimulationPlan(
+        num_paths=20000, seed=2), fixed, trace=True))
+    # the path split forced with more chains than ranks (SABR_T2_SHARD=paths), reference streams
+    os.environ["SABR_T2_SHARD"] = "paths"
+    out["case2_T2_paths"] = report_key(eng.calibrate_case2_T2(surf, None, s2, pkg.SimulationPlan(
+        num_paths=10000, seed=1, block_size=1000), fixed, trace=True))
+    del os.environ["SABR_T2_SHARD"]
     s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=4, workers=6, groups=2, t_min=0.1, seed=2)
     out["case2_formula"] = report_key(eng.calibrate_case2_formula(fx, None, s3, {"beta": 1.0}, trace=True))
     return out

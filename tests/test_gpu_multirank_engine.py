@@ -2,7 +2,10 @@
 sharing one GPU; per-level record all-gather over gloo through
 sabr_ctx_init_host_exchange instead of NCCL) must return bit-identical
 reports for every calibrator: chains are keyed by their global index and the
-merge is a lexicographic (value, chain) minimum (annealer.cpp:141-159)."""
+merge is a lexicographic (value, chain) minimum (annealer.cpp:141-159).  With
+fewer T_II chains than ranks (or SABR_T2_SHARD=paths) the ranks split the MC
+path tiles instead and all-gather the tile partials every SA step; the tile
+reduction order is the single-rank one, so those reports are identical too."""
 import json
 import os
 import socket
