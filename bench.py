@@ -230,6 +230,14 @@ def run_ours(args):
     evals_per_launch = evals_tot / klaunch_tot / world  # this rank's chains
     achieved = evals_per_launch * per_eval["flops"] / avg_launch_s / 1e12
     traffic = per_eval.get("dram_bytes_per_launch")
+    # the same kernel as FP64-pipe occupancy: every FP64-pipe instruction (DFMA,
+    # DADD, DMUL, DSETP, ...) per eval against the lane-instruction peak
+    # (= the DFMA FLOP peak / 2), i.e. ncu's sm__pipe_fp64_cycles_active view
+    pipe = None
+    if per_eval.get("pipe_instr"):
+        pa = evals_per_launch * per_eval["pipe_instr"] / avg_launch_s / 1e12
+        pipe = {"instr_per_eval": per_eval["pipe_instr"], "achieved_Tinstr_per_s": pa,
+                "peak_Tinstr_per_s": peak / 2, "frac": pa / (peak / 2)}
 
     sec = {}
     if rank == 0 and world == 1 and not args.no_secondary:
@@ -266,7 +274,8 @@ def run_ours(args):
                      "avg_launch_ms": avg_launch_s * 1e3, "launches": klaunch_tot,
                      "flops_per_eval": per_eval["flops"], "flops_source": per_eval["source"],
                      "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "
-                                    "MEASURED_PEAKS.json has no FP64 figure"},
+                                    "MEASURED_PEAKS.json has no FP64 figure",
+                     "fp64_pipe": pipe},
         "clocks": clocks.summary(),
     }
     if sec:
@@ -298,7 +307,8 @@ def fp64_flops_per_eval():
         with open(p) as f:
             d = json.load(f)
         return {"flops": d["c2_flops_per_eval"], "source": d["source"],
-                "dram_bytes_per_launch": d.get("c2_dram_bytes_per_launch")}
+                "dram_bytes_per_launch": d.get("c2_dram_bytes_per_launch"),
+                "pipe_instr": d.get("c2_fp64_pipe_instr_per_eval")}
     # ~1180 FP64-pipe instructions per eval at m = 19 (upper bound,
     # counts one FLOP per instruction)
     return {"flops": 1180.0, "source": "SURVEY.md 8(d) estimate (FP64-pipe instr, m=19)"}

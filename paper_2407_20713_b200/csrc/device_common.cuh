@@ -187,12 +187,102 @@ SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
     return fabs(x) > 700.0 ? sat : res;
 }
 
+// ---------------------------------------------------- table log / sqrt ---
+// Bit casts usable on host and device (the host builds of these functions are
+// the accuracy checks of tools/mathtab_check.cpp).
+SABR_HD uint64_t dbits(double x) {
+#ifdef __CUDA_ARCH__
+    return static_cast<uint64_t>(__double_as_longlong(x));
+#else
+    uint64_t u;
+    __builtin_memcpy(&u, &x, 8);
+    return u;
+#endif
+}
+SABR_HD double bitsd(uint64_t u) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(u));
+#else
+    double x;
+    __builtin_memcpy(&x, &u, 8);
+    return x;
+#endif
+}
+
+// log(x) for positive normal x: x = 2^k z with z in [0.6875, 1.375) (so z is
+// near 1 when x is), z in one of 128 intervals with centre c:
+// log x = k ln2 - log(invc) + log1p(r), r = z*invc - 1 (one FMA), |r| < 2^-7,
+// log1p by its degree-8 Taylor polynomial (truncation < 2^-60 |r|).  Table
+// entry i = {invc = RN(1/c), -log(invc) as hi (on a 2^-42 grid, so k ln2_hi +
+// hi is exact) + lo} (host long double,
+// kernels_mc.cu: log_table_host()); the two intervals around 1 (kLogOne - 1,
+// kLogOne) have invc = 1, -log(invc) = 0, so r = z - 1 exactly and nothing
+// cancels as log x -> 0.  <= 1 ulp (tools/mathtab_check.cpp); 16 FP64 ops, no
+// branch (libdevice log: 31 FP64 ops, 104 instructions).
+constexpr int kLogTableSize = 128;
+constexpr int kLogOne = 80;  // the interval that starts at z = 1: (bits(1) - bits(0.6875)) >> 45
+
+SABR_HD double log_tab(double x, const double4* __restrict__ tab) {
+    constexpr uint64_t kOff = 0x3fe6000000000000ull;  // 0.6875
+    constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;   // 11 trailing zero bits: k*kLn2Hi exact
+    constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
+    const uint64_t ix = dbits(x);
+    const uint64_t tmp = ix - kOff;
+    const int i = static_cast<int>((tmp >> 45) & (kLogTableSize - 1));
+    const int k = static_cast<int>(static_cast<int64_t>(tmp) >> 52);
+    const double z = bitsd(ix - (tmp & (0xfffull << 52)));
+    const double4 e = tab[i];
+    const double r = fma(z, e.x, -1.0);
+    const double kd = static_cast<double>(k);
+    const double t1 = fma(kd, kLn2Hi, e.y);
+    const double t2 = t1 + r;
+    const double lo = fma(kd, kLn2Lo, e.z) + ((t1 - t2) + r);
+    const double r2 = r * r;
+    const double p = fma(fma(fma(fma(fma(fma(fma(-1.0 / 8, r, 1.0 / 7), r, -1.0 / 6), r, 1.0 / 5), r, -1.0 / 4),
+                                     r, 1.0 / 3), r, -0.5), r2, lo);
+    return t2 + p;
+}
+
+// sqrt(a) for a >= 0 (finite): MUFU.RSQ64H seed, two Goldschmidt steps and a
+// final residual correction (<= 1 ulp; libdevice's IEEE sqrt has a slow-path
+// branch and 24 FP64 ops).  sqrt(0) = 0.
+SABR_HD double sqrt_pos(double a) {
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+#else
+    // host model of the hardware seed: 1/sqrt(a) truncated to 23 bits
+    const double y = bitsd(dbits(1.0 / __builtin_sqrt(a)) & ~((1ull << 29) - 1));
+#endif
+    double s = a * y, h = 0.5 * y;
+    double r = fma(-s, h, 0.5);
+    s = fma(s, r, s);
+    h = fma(h, r, h);
+    r = fma(-s, h, 0.5);
+    s = fma(s, r, s);
+    h = fma(h, r, h);
+    const double d = fma(-s, s, a);
+    s = fma(d, h, s);
+    return a > 0.0 ? s : 0.0;
+}
+
 // Box-Muller on two uniforms, proj/src/mc.cpp:30-36.  theta = 2*pi*u2 is
 // evaluated as sincospi(2*u2) (2*u2 is exact), i.e. without the rounding of
 // the 2*pi product; differences are below 1e-15 absolute in z.
 SABR_D void box_muller(double ua, double ub, double& z1, double& z2) {
     const double u1 = 1.0 - ua;
     const double r = sqrt(-2.0 * log(u1));
+    double s, c;
+    sincospi(2.0 * ub, &s, &c);
+    z1 = r * c;
+    z2 = r * s;
+}
+
+// The same with the table log and sqrt_pos (the MC path loops): u1 = 1 - U
+// lies in (2^-53, 1], a positive normal, and -2 log(u1) >= 0.
+SABR_D void box_muller_tab(double ua, double ub, const double4* __restrict__ logtab, double& z1, double& z2) {
+    const double u1 = 1.0 - ua;
+    const double r = sqrt_pos(-2.0 * log_tab(u1, logtab));
     double s, c;
     sincospi(2.0 * ub, &s, &c);
     z1 = r * c;

@@ -632,6 +632,13 @@ const double2* exp_table_device(sabr_ctx* ctx) {
     return upload(ctx, "exptab", std::vector<double2>(host, host + sabr_dev::kExpTableSize));
 }
 
+const double4* log_table_device(sabr_ctx* ctx) {
+    auto it = ctx->bufs.find("logtab");
+    if (it != ctx->bufs.end()) return static_cast<const double4*>(it->second.first);
+    const double4* host = log_table_host();
+    return upload(ctx, "logtab", std::vector<double4>(host, host + sabr_dev::kLogTableSize));
+}
+
 void* dev_buf(sabr_ctx* ctx, const std::string& key, size_t bytes) {
     auto& slot = ctx->bufs[key];
     if (slot.second < bytes) {
@@ -934,6 +941,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.strikes = upload(ctx, "mc_strikes", strikes);
     P.jump = upload(ctx, "mc_jump", jump);
     P.exptab = exp_table_device(ctx);
+    P.logtab = log_table_device(ctx);
     P.partials = static_cast<double*>(
         dev_buf(ctx, "mc_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * P.n_tiles));
     P.terminals = nullptr;
@@ -1503,6 +1511,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
         P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});
         P.jump = upload(ctx, "mc_jump", jump);
         P.exptab = exp_table_device(ctx);
+    P.logtab = log_table_device(ctx);
         P.partials = nullptr;
         P.terminals = static_cast<double*>(dev_buf(ctx, "mc_terminals", sizeof(double) * plan->num_paths));
         P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
@@ -1633,6 +1642,7 @@ SABR_API sabr_status sabr_mc_price_cliquet(sabr_ctx* ctx, int32_t model, const d
         P.strikes = upload(ctx, "mc_strikes", std::vector<double>{0.0});
         P.jump = upload(ctx, "mc_jump", jump);
         P.exptab = exp_table_device(ctx);
+    P.logtab = log_table_device(ctx);
         P.partials = static_cast<double*>(dev_buf(ctx, "mc_partials", sizeof(double) * 2 * P.n_tiles));
         P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
         check_cuda(cudaMemsetAsync(P.bad, 0, sizeof(int), ctx->stream), "memset bad");

@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     const int mq = sl.q_end - sl.q_begin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ double2 tab[kExpTableSize];
+    __shared__ double4 ltab[kLogTableSize];
     for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
+    for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
 
     // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
     // log space, F = F0 exp(x), alpha = exp(la):
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
                 } else {
                     philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
                 }
-                box_muller(ua, ub, z1, z2);
+                box_muller_tab(ua, ub, ltab, z1, z2);
             };
             // all candidates' log-Euler step with the shared normals; each
             // candidate's coefficients of the NEXT step are loaded right after
@@ -367,7 +369,9 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
                                                                  const __grid_constant__ CliquetSpecDev C) {
     __shared__ double acc[kWarps][2];
     __shared__ double2 tab[kExpTableSize];
+    __shared__ double4 ltab[kLogTableSize];
     for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
+    for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
     if (threadIdx.x < kWarps * 2) (&acc[0][0])[threadIdx.x] = 0.0;
     __syncthreads();
     const int tile = blockIdx.x;
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
                     philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
                 }
                 double z1, z2;
-                box_muller(ua, ub, z1, z2);
+                box_muller_tab(ua, ub, ltab, z1, z2);
                 const StepCoef q = P.coef[sl.step_off + i];
                 const double nh = exp_tab(logn ? la : fma(bm1, sl.lnf0 + x, la), tab);
                 la += fma(q.c1, z1, -q.c2);
@@ -541,6 +545,28 @@ const double2* exp_table_host() {
             const long double v = exp2l(static_cast<long double>(i) / kExpTableSize);
             const double hi = static_cast<double>(v);
             table[i] = make_double2(hi, static_cast<double>(v - static_cast<long double>(hi)));
+        }
+        built = true;
+    }
+    return table;
+}
+
+// {RN(1/c_i), -log(RN(1/c_i)) as hi + lo} for the 128 intervals of log_tab
+// (device_common.cuh), c_i the interval centre; x86 long double.
+const double4* log_table_host() {
+    static double4 table[kLogTableSize];
+    static bool built = false;
+    if (!built) {
+        for (int i = 0; i < kLogTableSize; ++i) {
+            const double c = bitsd(0x3fe6000000000000ull + (static_cast<uint64_t>(i) << 45) + (1ull << 44));
+            // the two intervals around 1 use invc = 1 exactly: r = z - 1 is then
+        // exact and nothing cancels as log x -> 0
+        const double invc = (i == kLogOne - 1 || i == kLogOne) ? 1.0
+                                                                : static_cast<double>(1.0L / static_cast<long double>(c));
+            const long double nl = -logl(static_cast<long double>(invc));
+            // hi on a 2^-42 grid: k*ln2_hi + hi is then exact for every |k| < 2^10
+        const double hi = static_cast<double>(roundl(nl * 0x1.0p42L) * 0x1.0p-42L);
+            table[i] = make_double4(invc, hi, static_cast<double>(nl - static_cast<long double>(hi)), 0.0);
         }
         built = true;
     }

@@ -1,0 +1,50 @@
+// Host build of the device log_tab / sqrt_pos (device_common.cuh) against
+// x86 long double: max error in ulps over Box-Muller's inputs u1 = 1 - k 2^-53
+// (all binades down to 2^-53) and random positive doubles.
+//   nvcc -x cu -O2 -std=c++17 -I include -I paper_2407_20713_b200/csrc tools/mathtab_check.cpp -o /tmp/mathtab_check
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "device_common.cuh"
+
+using namespace sabr_dev;
+
+static double4 g_tab[kLogTableSize];
+
+static double ulp_err(double got, long double want) {
+    const double w = static_cast<double>(want);
+    const double ulp = std::nextafter(std::fabs(w), INFINITY) - std::fabs(w);
+    return w == 0 ? std::fabs(got) : static_cast<double>(std::fabs(static_cast<long double>(got) - want) / ulp);
+}
+
+int main() {
+    for (int i = 0; i < kLogTableSize; ++i) {
+        const double c = bitsd(0x3fe6000000000000ull + (static_cast<uint64_t>(i) << 45) + (1ull << 44));
+        // the two intervals around 1 use invc = 1 exactly: r = z - 1 is then
+        // exact and nothing cancels as log x -> 0
+        const double invc = (i == kLogOne - 1 || i == kLogOne) ? 1.0
+                                                                : static_cast<double>(1.0L / static_cast<long double>(c));
+        const long double nl = -logl(static_cast<long double>(invc));
+        // hi on a 2^-42 grid: k*ln2_hi + hi is then exact for every |k| < 2^10
+        const double hi = static_cast<double>(roundl(nl * 0x1.0p42L) * 0x1.0p-42L);
+        g_tab[i] = double4{invc, hi, static_cast<double>(nl - static_cast<long double>(hi)), 0.0};
+    }
+    std::mt19937_64 gen(1);
+    double worst_log = 0, worst_sqrt = 0, worst_glibc = 0;
+    for (long n = 0; n < 20000000; ++n) {
+        // u1 = 1 - k 2^-53 with k spread over every binade
+        const int b = static_cast<int>(gen() % 54);
+        const uint64_t k = b == 0 ? 0 : ((gen() >> 11) >> (53 - b));
+        const double u1 = 1.0 - static_cast<double>(k) * 0x1.0p-53;
+        if (!(u1 > 0)) continue;
+        const long double want = logl(static_cast<long double>(u1));
+        worst_log = std::max(worst_log, ulp_err(log_tab(u1, g_tab), want));
+        worst_glibc = std::max(worst_glibc, ulp_err(std::log(u1), want));
+        const double a = -2.0 * std::log(u1);
+        worst_sqrt = std::max(worst_sqrt, ulp_err(sqrt_pos(a), sqrtl(static_cast<long double>(a))));
+    }
+    std::printf("log_tab max err %.3f ulp (glibc log %.3f ulp); sqrt_pos max err %.3f ulp; sqrt_pos(0) = %g\n",
+                worst_log, worst_glibc, worst_sqrt, sqrt_pos(0.0));
+    return worst_log < 1.0 && worst_sqrt < 1.0 && sqrt_pos(0.0) == 0.0 ? 0 : 1;
+}
