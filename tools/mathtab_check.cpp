@@ -4,6 +4,7 @@
 //   nvcc -x cu -O2 -std=c++17 -I include -I paper_2407_20713_b200/csrc tools/mathtab_check.cpp -o /tmp/mathtab_check
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "device_common.cuh"
@@ -18,7 +19,8 @@ static double ulp_err(double got, long double want) {
     return w == 0 ? std::fabs(got) : static_cast<double>(std::fabs(static_cast<long double>(got) - want) / ulp);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const long iters = argc > 1 ? std::atol(argv[1]) : 20000000;
     for (int i = 0; i < kLogTableSize; ++i) {
         const double c = bitsd(0x3fe6000000000000ull + (static_cast<uint64_t>(i) << 45) + (1ull << 44));
         // the two intervals around 1 use invc = 1 exactly: r = z - 1 is then
@@ -32,7 +34,7 @@ int main() {
     }
     std::mt19937_64 gen(1);
     double worst_log = 0, worst_sqrt = 0, worst_glibc = 0;
-    for (long n = 0; n < 20000000; ++n) {
+    for (long n = 0; n < iters; ++n) {
         // u1 = 1 - k 2^-53 with k spread over every binade
         const int b = static_cast<int>(gen() % 54);
         const uint64_t k = b == 0 ? 0 : ((gen() >> 11) >> (53 - b));
