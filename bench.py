@@ -166,11 +166,36 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     eng = pkg.Engine(local, stream=stream.cuda_stream)
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        uid = torch.zeros(129, dtype=torch.uint8, device=dev)  # NCCL unique id + "ok" byte
         if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(pkg.Engine.comm_unique_id()), dtype=torch.uint8))
+            try:
+                uid[:128].copy_(torch.frombuffer(bytearray(pkg.Engine.comm_unique_id()), dtype=torch.uint8))
+                uid[128] = 1
+            except pkg.SabrError:
+                pass
         dist.broadcast(uid, 0)
-        eng.init_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        ok = torch.tensor([0], dtype=torch.int32, device=dev)
+        try:
+            if int(uid[128]) != 1:
+                raise pkg.SabrError("no NCCL unique id on rank 0")
+            eng.init_comm(bytes(uid[:128].cpu().numpy().tobytes()), rank, world)
+            ok.fill_(1)
+        except pkg.SabrError as e:
+            print(f"rank {rank}: engine NCCL init failed ({e})", file=sys.stderr)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok) == 1:
+            transport = "NCCL all-gather (engine communicator)"
+        else:  # engine cannot open its own communicator: the records go through torch's NCCL group
+            def allgather(send: bytes) -> bytes:
+                t = torch.frombuffer(bytearray(send), dtype=torch.uint8).to(dev)
+                out = torch.empty(world * t.numel(), dtype=torch.uint8, device=dev)
+                dist.all_gather_into_tensor(out, t)
+                return bytes(out.cpu().numpy().tobytes())
+
+            eng.init_host_exchange(rank, world, allgather)
+            transport = "torch.distributed all-gather (host exchange)"
+    else:
+        transport = "none (1 rank)"
     eng.set_profiling(True)
 
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
@@ -263,7 +288,8 @@ def run_ours(args):
                    "cost_evals_per_step": evals_tot / args.steps,
                    "calibration_wall_s": t_wall / (args.steps * len(fx.slices)),
                    "l2": "flushed (256 MB write) before every timed step",
-                   "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather per level"},
+                   "parallelism": f"chains sharded over {world} GPU(s), one 240-byte record all-gather per level",
+                   "transport": transport},
         "e2e": {"value": e2e, "unit": "cost-evals/s",
                 "h2d_bytes_per_step": len(fx.slices) * (surface_bytes(pkg.VolSurface(fx.spot, [fx.slices[0]])) + 4 * 8 + 400),
                 "d2h_bytes_per_step": len(fx.slices) * (400 + 8 * LEVELS_C1 + 8 * 19 + 8 * 5)},
