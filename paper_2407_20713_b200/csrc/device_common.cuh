@@ -504,6 +504,41 @@ SABR_HD bool case2_feasible(const double* p) {
     return ok;
 }
 
+// case2_feasible by one warp: the 256 grid nodes split over the lanes (8
+// each), lane 0 adds the scalar checks and the two stationary points; the
+// verdict is the AND over the warp (order-free, so identical to the serial
+// predicate).  Every lane must pass the same p.
+SABR_D bool case2_feasible_warp(const double* p) {
+    const int lane = threadIdx.x & 31;
+    const double alpha = p[0], beta = p[1], a = p[8], b = p[9], horizon = p[10];
+    constexpr double kLo = -1 - 1e-9, kHi = 1 + 1e-9;
+    bool ok = (alpha > 0) && (beta >= 0 && beta <= 1) && (a >= 0 && b >= 0) && (horizon > 0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int i = 1 + lane + 32 * j;
+        const double t = horizon * i / 256;
+        const double r = case2_rho_at(p, t);
+        ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+    }
+    if (lane == 0) {
+        if (a > 0 && p[3] != 0) {
+            const double t = 1.0 / a - p[2] / p[3];
+            if (t > 0 && t <= horizon) {
+                const double r = case2_rho_at(p, t);
+                ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+            }
+        }
+        if (b > 0 && p[6] != 0) {
+            const double t = 1.0 / b - p[5] / p[6];
+            if (t > 0 && t <= horizon) {
+                const double r = case2_rho_at(p, t);
+                ok = ok && !(r < kLo || r > kHi) && !(case2_nu_at(p, t) <= 0);
+            }
+        }
+    }
+    return __all_sync(0xffffffffu, ok);
+}
+
 // ------------------------------------------------------ level merge rule ---
 
 // (value, global chain index) lexicographic order: strict '<' on the value

@@ -972,31 +972,47 @@ __global__ void t2_level_init_kernel(T2Chain* __restrict__ chains, const sabr_sa
     store_rng(r, ch.rng);
 }
 
-__global__ void t2_propose_kernel(T2Chain* __restrict__ chains, const sabr_sa_state* st,
-                                  const T2StepArgs a, double* __restrict__ alpha0,
-                                  double* __restrict__ beta, uint8_t* __restrict__ active) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= a.n_local) return;
+// One warp per chain: lane 0 proposes (its stored stream), the warp shares
+// the proposal and evaluates the 256-node feasibility grid together.
+constexpr int kProposeChainsPerCta = 4;
+
+__global__ void __launch_bounds__(32 * kProposeChainsPerCta)
+    t2_propose_kernel(T2Chain* __restrict__ chains, const sabr_sa_state* st, const T2StepArgs a,
+                      double* __restrict__ alpha0, double* __restrict__ beta, uint8_t* __restrict__ active) {
+    const int c = blockIdx.x * kProposeChainsPerCta + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= a.n_local) return;  // warp-uniform
     T2Chain& ch = chains[c];
-    ch.active = 0;
-    active[c] = 0;
-    if (st->done || ch.evals >= st->eval_cap) return;  // annealer.cpp:120
-    Xoshiro r;
-    load_rng(r, ch.rng);
-    const double ratio = a.temp / a.t0;
-    const double scale = (ratio < 1.0) ? ratio : 1.0;
-    double x[10], y[11];
-    for (int i = 0; i < 10; ++i) x[i] = ch.x[i];
-    propose_full(x, y, a.lo, a.hi, a.range, a.free_mask, scale, r);
-    store_rng(r, ch.rng);
+    if (st->done || ch.evals >= st->eval_cap) {  // annealer.cpp:120
+        if (lane == 0) {
+            ch.active = 0;
+            active[c] = 0;
+        }
+        return;
+    }
+    double y[11];
+    if (lane == 0) {
+        Xoshiro r;
+        load_rng(r, ch.rng);
+        const double ratio = a.temp / a.t0;
+        const double scale = (ratio < 1.0) ? ratio : 1.0;
+        double x[10];
+        for (int i = 0; i < 10; ++i) x[i] = ch.x[i];
+        propose_full(x, y, a.lo, a.hi, a.range, a.free_mask, scale, r);
+        store_rng(r, ch.rng);
+    }
+#pragma unroll
+    for (int i = 0; i < 10; ++i) y[i] = __shfl_sync(0xffffffffu, y[i], 0);
     y[10] = a.horizon;
-    for (int i = 0; i < 10; ++i) ch.y[i] = y[i];
     // SearchSpace::is_feasible -> case2_feasible (calibration.cpp:467-469)
-    const bool ok = case2_feasible(y);
-    ch.active = ok ? 1 : 0;
-    active[c] = ok ? 1 : 0;
-    alpha0[c] = y[0];
-    beta[c] = y[1];
+    const bool ok = case2_feasible_warp(y);
+    if (lane == 0) {
+        for (int i = 0; i < 10; ++i) ch.y[i] = y[i];
+        ch.active = ok ? 1 : 0;
+        active[c] = ok ? 1 : 0;
+        alpha0[c] = y[0];
+        beta[c] = y[1];
+    }
 }
 
 // coef[i][c] (step-major, cand_stride columns); inactive and padding
@@ -1264,7 +1280,8 @@ cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const
 cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
                               double* alpha0, double* beta, uint8_t* active, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
-    t2_propose_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, st, a, alpha0, beta, active);
+    t2_propose_kernel<<<(a.n_local + kProposeChainsPerCta - 1) / kProposeChainsPerCta, 32 * kProposeChainsPerCta, 0,
+                        s>>>(chains, st, a, alpha0, beta, active);
     return cudaGetLastError();
 }
 
