@@ -266,6 +266,35 @@ SABR_HD double sqrt_pos(double a) {
     return a > 0.0 ? s : 0.0;
 }
 
+// (sin 2 pi u, cos 2 pi u) for u in [0, 1): 2 pi u = (pi/64)(k + f) with
+// x = 128 u (exact), k = rint(x), f = x - k in [-1/2, 1/2] (exact); table
+// entry k mod 128 = {sin(pi k/64), cos(pi k/64)} (host long double,
+// kernels_mc.cu: sincos_table_host()); t = (pi/64) f in double-double
+// precision, sin t and cos t - 1 by Taylor polynomials (truncation < 1e-22
+// for |t| <= pi/128); recombined by the angle-addition formulas.
+// <= 1 ulp (tools/mathtab_check.cpp); branch-free (libdevice sincospi: 96
+// instructions).
+constexpr int kSinCosTableSize = 128;
+
+SABR_HD void sincos_2pi(double u, const double2* __restrict__ tab, double& s, double& c) {
+    constexpr double kPi64Hi = 0x1.921fb54442d18p-5;   // RN(pi/64)
+    constexpr double kPi64Lo = 0x1.1a62633145c07p-59;  // pi/64 - kPi64Hi
+    constexpr double kShift = 0x1.8p52;
+    const double x = u * 128.0;
+    const double kd = (x + kShift) - kShift;  // rint for 0 <= x < 2^51
+    const double f = x - kd;
+    const int k = static_cast<int>(kd) & (kSinCosTableSize - 1);
+    const double t = fma(f, kPi64Hi, f * kPi64Lo);
+    const double t2 = t * t;
+    const double ps = fma(fma(fma(t2, 1.0 / 362880, -1.0 / 5040), t2, 1.0 / 120), t2, -1.0 / 6);
+    const double st = fma(t * t2, ps, t);
+    const double pc = fma(fma(fma(t2, 1.0 / 40320, -1.0 / 720), t2, 1.0 / 24), t2, -0.5);
+    const double cm1 = t2 * pc;
+    const double2 e = tab[k];
+    s = e.x + fma(e.x, cm1, e.y * st);
+    c = e.y + fma(e.y, cm1, -(e.x * st));
+}
+
 // Box-Muller on two uniforms, proj/src/mc.cpp:30-36.  theta = 2*pi*u2 is
 // evaluated as sincospi(2*u2) (2*u2 is exact), i.e. without the rounding of
 // the 2*pi product; differences are below 1e-15 absolute in z.
@@ -278,13 +307,14 @@ SABR_D void box_muller(double ua, double ub, double& z1, double& z2) {
     z2 = r * s;
 }
 
-// The same with the table log and sqrt_pos (the MC path loops): u1 = 1 - U
-// lies in (2^-53, 1], a positive normal, and -2 log(u1) >= 0.
-SABR_D void box_muller_tab(double ua, double ub, const double4* __restrict__ logtab, double& z1, double& z2) {
+// The same with the table log, sqrt_pos and the table sincos (the MC path
+// loops): u1 = 1 - U lies in (2^-53, 1], a positive normal, -2 log(u1) >= 0.
+SABR_D void box_muller_tab(double ua, double ub, const double4* __restrict__ logtab,
+                           const double2* __restrict__ sctab, double& z1, double& z2) {
     const double u1 = 1.0 - ua;
     const double r = sqrt_pos(-2.0 * log_tab(u1, logtab));
     double s, c;
-    sincospi(2.0 * ub, &s, &c);
+    sincos_2pi(ub, sctab, s, c);
     z1 = r * c;
     z2 = r * s;
 }

@@ -632,6 +632,13 @@ const double2* exp_table_device(sabr_ctx* ctx) {
     return upload(ctx, "exptab", std::vector<double2>(host, host + sabr_dev::kExpTableSize));
 }
 
+const double2* sincos_table_device(sabr_ctx* ctx) {
+    auto it = ctx->bufs.find("sctab");
+    if (it != ctx->bufs.end()) return static_cast<const double2*>(it->second.first);
+    const double2* host = sincos_table_host();
+    return upload(ctx, "sctab", std::vector<double2>(host, host + sabr_dev::kSinCosTableSize));
+}
+
 const double4* log_table_device(sabr_ctx* ctx) {
     auto it = ctx->bufs.find("logtab");
     if (it != ctx->bufs.end()) return static_cast<const double4*>(it->second.first);
@@ -942,6 +949,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.jump = upload(ctx, "mc_jump", jump);
     P.exptab = exp_table_device(ctx);
     P.logtab = log_table_device(ctx);
+    P.sctab = sincos_table_device(ctx);
     P.partials = static_cast<double*>(
         dev_buf(ctx, "mc_partials", sizeof(double) * 2 * static_cast<size_t>(nq) * P.n_tiles));
     P.terminals = nullptr;
@@ -1512,6 +1520,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
         P.jump = upload(ctx, "mc_jump", jump);
         P.exptab = exp_table_device(ctx);
     P.logtab = log_table_device(ctx);
+    P.sctab = sincos_table_device(ctx);
         P.partials = nullptr;
         P.terminals = static_cast<double*>(dev_buf(ctx, "mc_terminals", sizeof(double) * plan->num_paths));
         P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
@@ -1643,6 +1652,7 @@ SABR_API sabr_status sabr_mc_price_cliquet(sabr_ctx* ctx, int32_t model, const d
         P.jump = upload(ctx, "mc_jump", jump);
         P.exptab = exp_table_device(ctx);
     P.logtab = log_table_device(ctx);
+    P.sctab = sincos_table_device(ctx);
         P.partials = static_cast<double*>(dev_buf(ctx, "mc_partials", sizeof(double) * 2 * P.n_tiles));
         P.bad = static_cast<int*>(dev_buf(ctx, "mc_bad", sizeof(int)));
         check_cuda(cudaMemsetAsync(P.bad, 0, sizeof(int), ctx->stream), "memset bad");

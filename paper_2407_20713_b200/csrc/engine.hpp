@@ -57,6 +57,7 @@ T* upload(sabr_ctx* ctx, const std::string& key, const std::vector<T>& v) {
 const double2* exp_table_device(sabr_ctx* ctx);
 // The log_tab table (Box-Muller's log in the MC kernels), uploaded once per context.
 const double4* log_table_device(sabr_ctx* ctx);
+const double2* sincos_table_device(sabr_ctx* ctx);
 // Upload one candidate's step coefficients (FP64, + FP32 copy for SABR_FP32).
 void set_coefficients(sabr_ctx* ctx, McParams& P, const std::vector<StepCoef>& coef, int precision);
 

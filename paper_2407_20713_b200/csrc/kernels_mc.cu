@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ double2 tab[kExpTableSize];
     __shared__ double4 ltab[kLogTableSize];
+    __shared__ double2 sctab[kSinCosTableSize];
     for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
     for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
+    for (int i = threadIdx.x; i < kSinCosTableSize; i += kMcThreads) sctab[i] = P.sctab[i];
 
     // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
     // log space, F = F0 exp(x), alpha = exp(la):
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
                 } else {
                     philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
                 }
-                box_muller_tab(ua, ub, ltab, z1, z2);
+                box_muller_tab(ua, ub, ltab, sctab, z1, z2);
             };
             // all candidates' log-Euler step with the shared normals; each
             // candidate's coefficients of the NEXT step are loaded right after
@@ -373,8 +375,10 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
     __shared__ double acc[kWarps][2];
     __shared__ double2 tab[kExpTableSize];
     __shared__ double4 ltab[kLogTableSize];
+    __shared__ double2 sctab[kSinCosTableSize];
     for (int i = threadIdx.x; i < kExpTableSize; i += kMcThreads) tab[i] = P.exptab[i];
     for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
+    for (int i = threadIdx.x; i < kSinCosTableSize; i += kMcThreads) sctab[i] = P.sctab[i];
     if (threadIdx.x < kWarps * 2) (&acc[0][0])[threadIdx.x] = 0.0;
     __syncthreads();
     const int tile = blockIdx.x;
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
                     philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
                 }
                 double z1, z2;
-                box_muller_tab(ua, ub, ltab, z1, z2);
+                box_muller_tab(ua, ub, ltab, sctab, z1, z2);
                 const StepCoef q = P.coef[sl.step_off + i];
                 const double nh = exp_tab(logn ? la : fma(bm1, sl.lnf0 + x, la), tab);
                 la += fma(q.c1, z1, -q.c2);
@@ -596,6 +600,19 @@ const double4* log_table_host() {
         const double hi = static_cast<double>(roundl(nl * 0x1.0p42L) * 0x1.0p-42L);
             table[i] = make_double4(invc, hi, static_cast<double>(nl - static_cast<long double>(hi)), 0.0);
         }
+        built = true;
+    }
+    return table;
+}
+
+// {sin(pi k/64), cos(pi k/64)}, k = 0..127, for sincos_2pi (device_common.cuh).
+const double2* sincos_table_host() {
+    static double2 table[kSinCosTableSize];
+    static bool built = false;
+    if (!built) {
+        const long double pi = 3.141592653589793238462643383279502884L;
+        for (int k = 0; k < kSinCosTableSize; ++k)
+            table[k] = make_double2(static_cast<double>(sinl(pi * k / 64)), static_cast<double>(cosl(pi * k / 64)));
         built = true;
     }
     return table;

@@ -56,6 +56,7 @@ struct McParams {
     int* bad;               // [n_cand] non-finite flag
     const double2* exptab;  // [128] 2^(i/128) double-double (exp_tab, device_common.cuh)
     const double4* logtab;  // [128] log_tab entries (Box-Muller's log, device_common.cuh)
+    const double2* sctab;   // [128] sincos_2pi entries (Box-Muller's angle)
     int32_t fp32;           // SABR_FP32: the FP32/MUFU path loop (coef32 instead of coef)
     const float4* coef32;   // [total_steps][cand_stride] {c1, c2, rs, ss} in FP32
 };
@@ -63,6 +64,7 @@ struct McParams {
 // The exp_tab and log_tab tables, built once on the host in long double.
 const double2* exp_table_host();
 const double4* log_table_host();
+const double2* sincos_table_host();
 
 // price_cliquet (mc.cpp:275-320): observation nodes (step counts) and their
 // F -> S factors exp(-(r-y)(T - t_node)).

@@ -119,6 +119,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     P.jump = upload(ctx, "t2_jump", jump);
     P.exptab = exp_table_device(ctx);
     P.logtab = log_table_device(ctx);
+    P.sctab = sincos_table_device(ctx);
     const double* d_market = upload(ctx, "t2_market", market);
     const double* d_tend = upload(ctx, "t2_tend", t_end);
     const double* d_dt = upload(ctx, "t2_dt", dt);

@@ -12,6 +12,7 @@
 using namespace sabr_dev;
 
 static double4 g_tab[kLogTableSize];
+static double2 g_sc[kSinCosTableSize];
 
 static double ulp_err(double got, long double want) {
     const double w = static_cast<double>(want);
@@ -32,7 +33,11 @@ int main(int argc, char** argv) {
         const double hi = static_cast<double>(roundl(nl * 0x1.0p42L) * 0x1.0p-42L);
         g_tab[i] = double4{invc, hi, static_cast<double>(nl - static_cast<long double>(hi)), 0.0};
     }
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < kSinCosTableSize; ++k)
+        g_sc[k] = double2{static_cast<double>(sinl(pi * k / 64)), static_cast<double>(cosl(pi * k / 64))};
     std::mt19937_64 gen(1);
+    double worst_sc = 0;  // absolute error in units of 2^-53 (the ulp at 1)
     double worst_log = 0, worst_sqrt = 0, worst_glibc = 0;
     for (long n = 0; n < iters; ++n) {
         // u1 = 1 - k 2^-53 with k spread over every binade
@@ -45,8 +50,16 @@ int main(int argc, char** argv) {
         worst_glibc = std::max(worst_glibc, ulp_err(std::log(u1), want));
         const double a = -2.0 * std::log(u1);
         worst_sqrt = std::max(worst_sqrt, ulp_err(sqrt_pos(a), sqrtl(static_cast<long double>(a))));
+        // Box-Muller's angle: u2 = (n >> 11) 2^-53
+        const double u2 = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+        double sn, cs;
+        sincos_2pi(u2, g_sc, sn, cs);
+        const long double th = 2 * pi * static_cast<long double>(u2);
+        worst_sc = std::max(worst_sc, static_cast<double>(fabsl(sn - sinl(th)) * 0x1.0p53L));
+        worst_sc = std::max(worst_sc, static_cast<double>(fabsl(cs - cosl(th)) * 0x1.0p53L));
     }
-    std::printf("log_tab max err %.3f ulp (glibc log %.3f ulp); sqrt_pos max err %.3f ulp; sqrt_pos(0) = %g\n",
-                worst_log, worst_glibc, worst_sqrt, sqrt_pos(0.0));
-    return worst_log < 1.0 && worst_sqrt < 1.0 && sqrt_pos(0.0) == 0.0 ? 0 : 1;
+    std::printf("log_tab max err %.3f ulp (glibc log %.3f ulp); sqrt_pos max err %.3f ulp; sqrt_pos(0) = %g; "
+                "sincos_2pi max abs err %.3f x 2^-53\n",
+                worst_log, worst_glibc, worst_sqrt, sqrt_pos(0.0), worst_sc);
+    return worst_log < 1.0 && worst_sqrt < 1.0 && sqrt_pos(0.0) == 0.0 && worst_sc < 1.0 ? 0 : 1;
 }
