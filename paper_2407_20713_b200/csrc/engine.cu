@@ -267,6 +267,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     a.state = static_cast<sabr_sa_state*>(dev_buf(ctx, "sa_state", sizeof(sabr_sa_state)));
     a.block_recs = static_cast<sabr_level_record*>(
         dev_buf(ctx, "sa_block_recs", sizeof(sabr_level_record) * grid));
+    a.block_sum = static_cast<BlockSummary*>(dev_buf(ctx, "sa_block_sum", sizeof(BlockSummary) * grid));
     a.rank_rec = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_rank_rec", sizeof(sabr_level_record)));
     auto* recv = static_cast<sabr_level_record*>(
         dev_buf(ctx, "sa_recv_recs", sizeof(sabr_level_record) * ctx->nranks));

@@ -30,6 +30,18 @@ enum ObjectiveKind : int32_t {
     OBJ_BUILTIN = 2,  // test_annealer.cpp closed forms
 };
 
+// The arg-min part of a CTA's level record, contiguous per CTA so the last
+// CTA's reduction reads three 16-byte vectors per record (the points stay in
+// the full sabr_level_record and are read for the two winners only).
+struct __align__(16) BlockSummary {
+    double end_value;
+    long long end_chain;
+    double best_value;
+    long long best_chain;
+    long long evals;
+    long long pad;
+};
+
 struct SaLevelArgs {
     double lo[SABR_MAX_DIM];
     double hi[SABR_MAX_DIM];
@@ -52,6 +64,7 @@ struct SaLevelArgs {
     int64_t levels_total;
     sabr_sa_state* state;        // device
     sabr_level_record* block_recs;  // [grid] scratch
+    BlockSummary* block_sum;        // [grid] scratch (arg-min fields of block_recs)
     sabr_level_record* rank_rec;    // [1] this rank's record (NCCL send buffer)
     unsigned int* ticket;           // [1] zero-initialised
     double* trace_f;                // [levels_total] device

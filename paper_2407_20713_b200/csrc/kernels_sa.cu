@@ -495,6 +495,8 @@ __device__ bool publish_block_record(RedShared<NT>& rs, sabr_level_record& rec,
         rec.best_chain = rs.b_win.i == LLONG_MAX ? -1 : rs.b_win.i;
         rec.evals = rs.n_tot;
         a.block_recs[blockIdx.x] = rec;
+        a.block_sum[blockIdx.x] = BlockSummary{rec.end_value, rec.end_chain, rec.best_value, rec.best_chain,
+                                               rec.evals, 0};
         __threadfence();
         const unsigned t = atomicAdd(a.ticket, 1u);
         rs.is_last = (t == gridDim.x - 1);
@@ -512,30 +514,32 @@ __device__ void reduce_block_records(RedShared<NT>& rs, const SaLevelArgs& a, in
     ArgMin ee{CUDART_INF, LLONG_MAX, -1}, bb{CUDART_INF, LLONG_MAX, -1};
     long long nn = 0;
     const int nrec = static_cast<int>(gridDim.x);
-    for (int k0 = threadIdx.x; k0 < nrec; k0 += 4 * NT) {
-        double rev[4], rbv[4];
-        long long rei[4], rbi[4], rn[4];
+    // 16 summaries in flight per thread: the scan is L2-latency bound and
+    // runs in one CTA while the rest of the GPU is idle
+    constexpr int U = 16;
+    for (int k0 = threadIdx.x; k0 < nrec; k0 += U * NT) {
+        double4 v[U];
+        long long n[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int k = k0 + u * NT;
-            rei[u] = rbi[u] = -1;
-            rn[u] = 0;
-            rev[u] = rbv[u] = CUDART_INF;
+            v[u] = make_double4(CUDART_INF, __longlong_as_double(-1ll), CUDART_INF, __longlong_as_double(-1ll));
+            n[u] = 0;
             if (k < nrec) {
-                const sabr_level_record* r = a.block_recs + k;
-                rev[u] = __ldcg(&r->end_value);
-                rei[u] = __ldcg(reinterpret_cast<const long long*>(&r->end_chain));
-                rbv[u] = __ldcg(&r->best_value);
-                rbi[u] = __ldcg(reinterpret_cast<const long long*>(&r->best_chain));
-                rn[u] = __ldcg(reinterpret_cast<const long long*>(&r->evals));
+                const double4* p = reinterpret_cast<const double4*>(a.block_sum + k);
+                const double2 lo = __ldcg(reinterpret_cast<const double2*>(p));
+                const double2 hi = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+                v[u] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                n[u] = __ldcg(&a.block_sum[k].evals);
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int k = k0 + u * NT;
-            if (rei[u] >= 0) argmin_combine(ee, ArgMin{rev[u], rei[u], k});
-            if (rbi[u] >= 0) argmin_combine(bb, ArgMin{rbv[u], rbi[u], k});
-            nn += rn[u];
+            const long long ei = __double_as_longlong(v[u].y), bi = __double_as_longlong(v[u].w);
+            if (ei >= 0) argmin_combine(ee, ArgMin{v[u].x, ei, k});
+            if (bi >= 0) argmin_combine(bb, ArgMin{v[u].z, bi, k});
+            nn += n[u];
         }
     }
     block_reduce(rs, ee, bb, nn);

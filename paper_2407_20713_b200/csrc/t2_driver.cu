@@ -158,6 +158,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     const int64_t grid = std::max<int64_t>(1, (n_local + t2_block_threads() - 1) / t2_block_threads());
     a.state = static_cast<sabr_sa_state*>(dev_buf(ctx, "sa_state", sizeof(sabr_sa_state)));
     a.block_recs = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_block_recs", sizeof(sabr_level_record) * grid));
+    a.block_sum = static_cast<BlockSummary*>(dev_buf(ctx, "sa_block_sum", sizeof(BlockSummary) * grid));
     a.rank_rec = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_rank_rec", sizeof(sabr_level_record)));
     auto* recv = static_cast<sabr_level_record*>(dev_buf(ctx, "sa_recv_recs", sizeof(sabr_level_record) * ctx->nranks));
     a.ticket = static_cast<unsigned int*>(dev_buf(ctx, "sa_ticket", sizeof(unsigned int)));
