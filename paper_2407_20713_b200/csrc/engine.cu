@@ -670,7 +670,8 @@ void Timer::start() {
     if (ctx->profiling) check_cuda(cudaEventRecord(ctx->ev0, ctx->stream), "event record");
 }
 void Timer::before() {
-    if (!ctx->profiling) return;
+    sampling = ctx->profiling && (calls++ % kSample == 0);
+    if (!sampling) return;
     if (ctx->kev_used + 2 > ctx->kev.size()) {
         for (int i = 0; i < 256; ++i) {
             cudaEvent_t e;
@@ -681,7 +682,7 @@ void Timer::before() {
     check_cuda(cudaEventRecord(ctx->kev[ctx->kev_used++], ctx->stream), "event record");
 }
 void Timer::after() {
-    if (!ctx->profiling) return;
+    if (!sampling) return;
     check_cuda(cudaEventRecord(ctx->kev[ctx->kev_used++], ctx->stream), "event record");
 }
 void Timer::stop(double units, double path_steps, int64_t kernel_launches, int64_t total_launches) {
@@ -697,12 +698,13 @@ void Timer::stop(double units, double path_steps, int64_t kernel_launches, int64
         check_cuda(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "event elapsed");
         t.total_ms = ms;
         double kms = 0.0;
-        for (size_t i = 0; i + 1 < ctx->kev_used; i += 2) {
+        size_t pairs = 0;
+        for (size_t i = 0; i + 1 < ctx->kev_used; i += 2, ++pairs) {
             float k = 0.f;
             check_cuda(cudaEventElapsedTime(&k, ctx->kev[i], ctx->kev[i + 1]), "event elapsed");
             kms += k;
         }
-        t.kernel_ms = ctx->kev_used ? kms : ms;
+        t.kernel_ms = pairs ? kms / pairs * static_cast<double>(calls) : ms;
     } else {
         t.total_ms = t.kernel_ms = 1e3 * seconds_since(t0);
     }

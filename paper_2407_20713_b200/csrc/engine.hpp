@@ -121,9 +121,16 @@ void allgather(sabr_ctx* ctx, const void* send, void* recv, size_t bytes);
 // Whole-call device time (events on the context stream) plus, when
 // profiling, the summed duration of each dominant-kernel launch bracketed by
 // its own event pair (before()/after()).
+// Per-launch CUDA events (profiling mode) around one in kSample launches of
+// the dominant kernel: events between kernels serialise them, so sampling
+// keeps programmatic dependent launch (kernels_sa.cu) effective for the rest;
+// kernel_ms is the sampled mean duration times the launch count.
 struct Timer {
+    static constexpr int64_t kSample = 8;
     sabr_ctx* ctx;
     std::chrono::steady_clock::time_point t0;
+    int64_t calls = 0;
+    bool sampling = false;
     explicit Timer(sabr_ctx* c);
     void start();
     void before();

@@ -565,6 +565,11 @@ __device__ void reduce_block_records(RedShared<NT>& rs, const SaLevelArgs& a, in
     }
 }
 
+// griddepcontrol (sm_90+): let the dependent grid launch / wait for the
+// prerequisite grid's completion and memory.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // --------------------------------------------------------- level kernel ---
 // propose, annealer.cpp:60-74, for one coordinate: bit-identical to the
 // reference (2u - 1 via Xoshiro::sym, the reflections use the host-doubled
@@ -723,7 +728,12 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
     __shared__ double bp_s[C][DIMF][NT];
 
     sabr_sa_state* st = a.state;
-    if (st->done) return;
+    // Programmatic dependent launch: the next level's grid may start as soon
+    // as SMs free up; everything before pdl_wait() (table and grid staging,
+    // the chains' stream seeding) does not depend on the previous level and
+    // overlaps its tail (the last CTA's merge).  Nothing written by the
+    // previous level is read before pdl_wait().
+    pdl_trigger();
     stage_exp(sv, tab_s);
     PGrid g = stage_pgrid(sv, smem);
     __syncthreads();
@@ -731,12 +741,17 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
 
     bool active[C];
     int64_t chain[C];
+    Xoshiro rng[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int64_t local = static_cast<int64_t>(blockIdx.x) * (NT * C) + c * NT + threadIdx.x;
         active[c] = local < a.n_local;
         chain[c] = a.chain_begin + local;
+        // substream keyed by (seed, level, chain): annealer.cpp:112-115
+        rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
     }
+    pdl_wait();
+    if (st->done) return;  // early-stopped run (max_evals): uniform exit
     double x[C][DIMF], y[C][DIMF], fx[C], bv[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -751,10 +766,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
     if (active[0]) {  // chain c > 0 active implies chain 0 active
         const long long cap64 = st->eval_cap;
         steps = cap64 < a.chain_length ? static_cast<int>(cap64 < 0 ? 0 : cap64) : a.chain_length;
-        Xoshiro rng[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-            rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
         const double ratio = temp / a.t0;
         const double scale = (ratio < 1.0) ? ratio : 1.0;
         double step_scale[DIMF];
@@ -1140,6 +1151,15 @@ bool multi_chain_enabled() {
     return on;
 }
 
+// SABR_SA_PDL=0 launches the level kernels without programmatic dependent launch.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SABR_SA_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
@@ -1160,8 +1180,17 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
             auto k = all_free ? sa_level_multi_kernel<KIND, DIMF, true> : sa_level_multi_kernel<KIND, DIMF, false>;
             cudaError_t e = set_smem(k, smem);
             if (e != cudaSuccess) return e;
-            k<<<grid, kPairThreads, smem, s>>>(sv, a, level, temp, inv_temp);
-            return cudaGetLastError();
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(kPairThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, k, sv, a, level, temp, inv_temp);
         }
     }
     if (all_free)
