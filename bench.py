@@ -392,6 +392,19 @@ def secondary(eng, torch, dev, stream):
             "precision": precision, "seconds": secs, "final_cost": rep.final_cost,
             "sample": "one SA step (L=1, one level) of 2048 chains; C5 names 1e6 chains over 8 GPUs "
                       "(125000 per GPU, ~61x this sample per GPU-step)"}
+    # C1 (BASELINE.json configs[0]): the reference's own CPU-sized case, static T_I on one EURO STOXX 50
+    # slice with the acceptance schedule (32 chains, 412 levels, 1,000,001 evals): latency-bound on a GPU
+    eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
+    s1 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=1)
+    eng.calibrate_static_T1(eq, 0, None, s1, None)
+    e0.record(stream)
+    rep = eng.calibrate_static_T1(eq, 0, None, s1, None)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    secs = e0.elapsed_time(e1) / 1e3
+    out["c1_static_calibration"] = {"metric": "calibrate_static_T1 wall time, C1 (EURO STOXX 50 slice 0, 32 chains)",
+                                    "unit": "s", "value": secs, "cost_evals": rep.evals - 1,
+                                    "cost_evals_per_s": (rep.evals - 1) / secs, "final_cost": rep.final_cost}
     # C3: Case I joint calibration, EUR/USD, beta = 1 (acceptance.cpp:317-339 schedule, 1e5 chains)
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
     s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8, t_min=1e-7,
