@@ -392,6 +392,25 @@ def secondary(eng, torch, dev, stream):
             "precision": precision, "seconds": secs, "final_cost": rep.final_cost,
             "sample": "one SA step (L=1, one level) of 2048 chains; C5 names 1e6 chains over 8 GPUs "
                       "(125000 per GPU, ~61x this sample per GPU-step)"}
+    # MC European pricing in the paper's shape (SSabr, 2^24 paths, 123 + 1 steps of
+    # 1/250 to T = 0.4959), through price_european_batch; the paper's GTX470 did 2.18e8 (FP64) and
+    # 1.62e9 (FP32) path-steps/s on this workload
+    p_reg = pkg.StaticSabrParams(0.375162, 0.999999, 0.331441, -0.999999)
+    for precision in ("fp64", "fp32"):
+        plan = pkg.SimulationPlan(num_paths=1 << 24, seed=5, rng="xoshiro", precision=precision)
+        eng.price_european_batch(p_reg, 2257.37, [2257.37], 0.018196, 0.034516, 0.495890, plan)
+        flush_l2(torch, dev)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        est = eng.price_european_batch(p_reg, 2257.37, [2257.37], 0.018196, 0.034516, 0.495890, plan)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        secs = e0.elapsed_time(e1) / 1e3
+        ps = float(plan.num_paths) * 124
+        out["mc_european_pricing" + ("" if precision == "fp64" else "_fp32")] = {
+            "metric": f"MC SABR path-steps/s (price_european_batch, 2^24 paths x 124 steps, {precision})",
+            "unit": "path-steps/s", "value": ps / secs, "seconds": secs, "price": est[0].value,
+            "std_error": est[0].std_error, "paper_gtx470_path_steps_per_s": 2.18e8 if precision == "fp64" else 1.62e9}
     # C1 (BASELINE.json configs[0]): the reference's own CPU-sized case, static T_I on one EURO STOXX 50
     # slice with the acceptance schedule (32 chains, 412 levels, 1,000,001 evals): latency-bound on a GPU
     eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
