@@ -194,6 +194,19 @@ def run_ours(args):
 
             eng.init_host_exchange(rank, world, allgather)
             transport = "torch.distributed all-gather (host exchange)"
+        # fused peer-memory exchange of the level records (CUDA IPC mailboxes over NVLink /
+        # NVSwitch, merged inside the level kernel): used when every rank can map the others
+        ok = torch.tensor([1], dtype=torch.int32, device=dev)
+        try:
+            eng.enable_peer_exchange()
+        except pkg.SabrError as e:
+            print(f"rank {rank}: peer exchange unavailable ({e})", file=sys.stderr)
+            ok.fill_(0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok) == 1:
+            transport = "fused peer-memory exchange in the level kernel (CUDA IPC mailboxes)"
+        else:
+            eng.disable_peer_exchange()
     else:
         transport = "none (1 rank)"
     eng.set_profiling(True)

@@ -213,6 +213,19 @@ typedef int (*sabr_allgather_fn)(void* user, const void* send, void* recv, int64
 SABR_API sabr_status sabr_ctx_init_host_exchange(sabr_ctx* ctx, int32_t rank, int32_t nranks,
                                                  sabr_allgather_fn fn, void* user);
 
+/* Fused peer-memory exchange for the T_I calibrators (after init_comm or
+ * init_host_exchange, which carry the one-time exchange of CUDA IPC handles):
+ * the last CTA of each rank's level kernel stores the 240-byte level record
+ * into every rank's mailbox over NVLink / NVSwitch peer memory, waits for the
+ * peers' records and merges them itself - no NCCL call, no separate merge
+ * kernel per level.  Needs peer access between the ranks' GPUs (or ranks on
+ * one GPU) and at most 16 ranks; results are identical to the other
+ * transports.  Other calibrators keep using the transport. */
+SABR_API sabr_status sabr_ctx_enable_peer_exchange(sabr_ctx* ctx);
+/* Back to the transport for every calibrator (e.g. when another rank could
+ * not enable the peer exchange: all ranks must use the same path). */
+SABR_API sabr_status sabr_ctx_disable_peer_exchange(sabr_ctx* ctx);
+
 /* ---- calibration (proj/include/sabr/calibration.hpp) -------------------- */
 
 /* calibrate_static_T1, calibration.hpp:82-85 / proj/src/calibration.cpp:289-323 */

@@ -453,6 +453,14 @@ class Engine:
         self._check(self.lib.sabr_ctx_init_host_exchange(self._ctx, C.c_int32(rank), C.c_int32(nranks),
                                                          self._exchange_cb, None))
 
+    def enable_peer_exchange(self) -> None:
+        """Fused peer-memory exchange of the T_I level records (after
+        init_comm / init_host_exchange); see include/sabr_b200.h."""
+        self._check(self.lib.sabr_ctx_enable_peer_exchange(self._ctx))
+
+    def disable_peer_exchange(self) -> None:
+        self._check(self.lib.sabr_ctx_disable_peer_exchange(self._ctx))
+
     def calibrate_static_T1(self, surface: VolSurface, slice: int, bounds=None,
                             schedule: Optional[AnnealingSchedule] = None, fixed=None,
                             trace: bool = False) -> CalibrationReport:

@@ -216,7 +216,8 @@ using LevelFn = std::function<cudaError_t(const SaLevelArgs&, int64_t, double)>;
 T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std::vector<double>& lo,
                      const std::vector<double>& hi, const std::vector<double>& start_full,
                      const sabr_schedule& sch, bool start_ok, int64_t records,
-                     const StartFn& start, const LevelFn& level_fn, int builtin, int pred) {
+                     const StartFn& start, const LevelFn& level_fn, int builtin, int pred,
+                     bool use_peer = false) {
     validate_schedule(sch);
     // SearchSpace::validate, annealer.cpp:48-58
     if (free_mask == 0) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
@@ -283,6 +284,16 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     }
     check_cuda(start(a), "sa_start");
 
+    // fused peer exchange (all ranks decide alike: every rank has chains iff n_chains >= nranks)
+    const bool peer = ctx->peer && ctx->nranks > 1 && n_chains >= ctx->nranks && use_peer;
+    if (peer) {
+        a.peer_boxes = ctx->peer_boxes;
+        a.my_rank = ctx->rank;
+        a.epoch_base = ctx->peer_epoch;
+        a.peer_error = ctx->peer_error;
+        ctx->peer_epoch += static_cast<unsigned long long>(L);
+    }
+
     Timer timer(ctx);
     timer.start();
     int64_t launched = 0;
@@ -294,7 +305,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
             timer.after();
             ++launched;
         }
-        if (ctx->nranks > 1) {
+        if (ctx->nranks > 1 && !peer) {
             allgather(ctx, a.rank_rec, recv, sizeof(sabr_level_record));
             check_cuda(launch_sa_merge(a, recv, level, ctx->stream), "sa_merge");
         }
@@ -309,6 +320,11 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     check_cuda(cudaMemcpyAsync(&out, a.state, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream), "D2H state");
     sync(ctx);
     timer.stop(static_cast<double>(out.evals - 1), 0.0, launched, launched);
+    if (peer) {
+        int err = 0;
+        check_cuda(cudaMemcpy(&err, ctx->peer_error, sizeof(int), cudaMemcpyDeviceToHost), "D2H peer error");
+        if (err) fail(SABR_E_NCCL, "peer exchange: a rank's level record did not arrive within 20 s");
+    }
 
     T1Out r;
     r.best_full.assign(out.best, out.best + dim_full);
@@ -339,7 +355,7 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
         [&](const SaLevelArgs& a, int64_t level, double temp) {
             return launch_sa_level(kind, sv, a, level, temp, s);
         },
-        builtin, pred);
+        builtin, pred, /*use_peer=*/true);
 }
 
 // GaussLegendreRule(n), proj/src/quadrature.cpp:13-33 (same Newton iteration,
@@ -1023,6 +1039,8 @@ SABR_API void sabr_ctx_destroy(sabr_ctx* ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto e : ctx->kev) cudaEventDestroy(e);
+    for (void* p : ctx->peer_opened) cudaIpcCloseMemHandle(p);
+    if (ctx->peer_box) cudaFree(ctx->peer_box);
     if (ctx->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(ctx->comm));
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1061,6 +1079,54 @@ SABR_API sabr_status sabr_ctx_init_host_exchange(sabr_ctx* ctx, int32_t rank, in
         ctx->nranks = nranks;
         ctx->exchange = nranks > 1 ? fn : nullptr;
         ctx->exchange_user = user;
+    });
+}
+
+SABR_API sabr_status sabr_ctx_enable_peer_exchange(sabr_ctx* ctx) {
+    return guarded([&] {
+        CtxLock l(ctx);
+        if (ctx->nranks <= 1) return;  // nothing to exchange
+        if (ctx->nranks > kMaxPeerRanks) fail(SABR_E_INVALID, "peer exchange: at most 16 ranks");
+        if (!ctx->comm && !ctx->exchange) fail(SABR_E_INVALID, "peer exchange: initialise a transport first");
+        if (ctx->peer) return;
+        PeerMailbox* box = nullptr;
+        check_cuda(cudaMalloc(&box, sizeof(PeerMailbox)), "cudaMalloc mailbox");
+        check_cuda(cudaMemset(box, 0, sizeof(PeerMailbox)), "memset mailbox");
+        cudaIpcMemHandle_t h;
+        check_cuda(cudaIpcGetMemHandle(&h, box), "cudaIpcGetMemHandle");
+        // one all-gather of the 64-byte handles over the existing transport
+        auto* dsend = static_cast<unsigned char*>(dev_buf(ctx, "peer_h_send", sizeof(h)));
+        auto* drecv = static_cast<unsigned char*>(dev_buf(ctx, "peer_h_recv", sizeof(h) * ctx->nranks));
+        check_cuda(cudaMemcpyAsync(dsend, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream), "H2D handle");
+        allgather(ctx, dsend, drecv, sizeof(h));
+        std::vector<cudaIpcMemHandle_t> all(ctx->nranks);
+        check_cuda(cudaMemcpyAsync(all.data(), drecv, sizeof(h) * ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H handles");
+        sync(ctx);
+        std::vector<PeerMailbox*> ptrs(ctx->nranks, nullptr);
+        for (int r = 0; r < ctx->nranks; ++r) {
+            if (r == ctx->rank) {
+                ptrs[r] = box;
+                continue;
+            }
+            void* p = nullptr;
+            check_cuda(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            ctx->peer_opened.push_back(p);
+            ptrs[r] = static_cast<PeerMailbox*>(p);
+        }
+        ctx->peer_boxes = upload(ctx, "peer_boxes", ptrs);
+        ctx->peer_error = static_cast<int*>(dev_buf(ctx, "peer_error", sizeof(int)));
+        check_cuda(cudaMemsetAsync(ctx->peer_error, 0, sizeof(int), ctx->stream), "memset");
+        sync(ctx);
+        ctx->peer_box = box;
+        ctx->peer = true;
+    });
+}
+
+SABR_API sabr_status sabr_ctx_disable_peer_exchange(sabr_ctx* ctx) {
+    return guarded([&] {
+        CtxLock l(ctx);
+        ctx->peer = false;
     });
 }
 

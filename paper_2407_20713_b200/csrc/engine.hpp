@@ -27,6 +27,13 @@ struct sabr_ctx {
     // host-side record exchange instead of NCCL (sabr_ctx_init_host_exchange)
     sabr_allgather_fn exchange = nullptr;
     void* exchange_user = nullptr;
+    // fused peer-memory exchange of the T_I level records (sabr_ctx_enable_peer_exchange)
+    bool peer = false;
+    sabr_gpu::PeerMailbox* peer_box = nullptr;          // this rank's mailbox (IPC-exported)
+    std::vector<void*> peer_opened;           // peers' mailboxes mapped into this process
+    sabr_gpu::PeerMailbox* const* peer_boxes = nullptr;  // device array [nranks]
+    int* peer_error = nullptr;
+    unsigned long long peer_epoch = 0;
     // grow-only device scratch, keyed by purpose
     std::map<std::string, std::pair<void*, size_t>> bufs;
     // host cache of xoshiro jump tables keyed by (draws per entry, count)

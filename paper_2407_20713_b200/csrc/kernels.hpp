@@ -42,6 +42,19 @@ struct __align__(16) BlockSummary {
     long long pad;
 };
 
+// Per-rank mailbox of the fused peer exchange (sabr_ctx_enable_peer_exchange):
+// every rank's last CTA stores its level record into slot [level parity][its
+// rank] of every rank's mailbox over NVLink / NVSwitch peer memory, then
+// raises the slot's epoch; a rank merges once all epochs of its own mailbox
+// show the level.  Two parities: a rank can be at most one level ahead of a
+// slower peer (its next merge needs the peer's next record), so a record is
+// never overwritten before the slower peer has read it.
+constexpr int kMaxPeerRanks = 16;
+struct PeerMailbox {
+    sabr_level_record rec[2][kMaxPeerRanks];
+    unsigned long long epoch[2][kMaxPeerRanks];
+};
+
 struct SaLevelArgs {
     double lo[SABR_MAX_DIM];
     double hi[SABR_MAX_DIM];
@@ -67,6 +80,10 @@ struct SaLevelArgs {
     BlockSummary* block_sum;        // [grid] scratch (arg-min fields of block_recs)
     sabr_level_record* rank_rec;    // [1] this rank's record (NCCL send buffer)
     unsigned int* ticket;           // [1] zero-initialised
+    PeerMailbox* const* peer_boxes; // [nranks] mailboxes (peer pointers) or null: fused exchange
+    int32_t my_rank;                // this rank (peer exchange)
+    unsigned long long epoch_base;  // level l publishes epoch epoch_base + l + 1
+    int* peer_error;                // set when the exchange timed out
     double* trace_f;                // [levels_total] device
 };
 

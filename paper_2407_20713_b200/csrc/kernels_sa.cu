@@ -505,6 +505,54 @@ __device__ bool publish_block_record(RedShared<NT>& rs, sabr_level_record& rec,
     return rs.is_last != 0;
 }
 
+// The fused cross-rank exchange of one level record (thread 0 of the last
+// CTA): store it into this rank's slot of every rank's mailbox (peer memory
+// over NVLink / NVSwitch; the own mailbox is local), fence system-wide, raise
+// the slot's epoch, wait until every slot of the own mailbox carries this
+// level's epoch, then apply merge_level to the records in rank order - the
+// all-gather and the merge of the NCCL path (sa_merge_kernel) without leaving
+// the level kernel.  A 20 s timeout turns a lost peer into an error (run
+// stopped, peer_error set) instead of a hang.
+__device__ __noinline__ void peer_exchange_and_merge(const SaLevelArgs& a, const sabr_level_record& out,
+                                                     int64_t level, int dim) {
+    const unsigned long long epoch = a.epoch_base + static_cast<unsigned long long>(level) + 1ull;
+    const int par = static_cast<int>(epoch & 1ull);
+    for (int r = 0; r < a.nranks; ++r) a.peer_boxes[r]->rec[par][a.my_rank] = out;
+    __threadfence_system();
+    for (int r = 0; r < a.nranks; ++r)
+        atomicExch(&a.peer_boxes[r]->epoch[par][a.my_rank], epoch);
+    PeerMailbox* own = a.peer_boxes[a.my_rank];
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < a.nranks; ++r) {
+        while (atomicAdd(&own->epoch[par][r], 0ull) < epoch) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 20000000000ull) {  // 20 s
+                atomicExch(a.peer_error, 1);
+                a.state->done = 1;
+                return;
+            }
+            __nanosleep(100);
+        }
+    }
+    __threadfence_system();
+    sabr_level_record recs[kMaxPeerRanks];
+    for (int r = 0; r < a.nranks; ++r) {
+        const volatile sabr_level_record* src = &own->rec[par][r];
+        recs[r].end_value = src->end_value;
+        recs[r].end_chain = src->end_chain;
+        recs[r].best_value = src->best_value;
+        recs[r].best_chain = src->best_chain;
+        recs[r].evals = src->evals;
+        for (int i = 0; i < SABR_MAX_DIM; ++i) {
+            recs[r].end_point[i] = src->end_point[i];
+            recs[r].best_point[i] = src->best_point[i];
+        }
+    }
+    merge_level(a.state, recs, a.nranks, a.n_chains, a.max_evals, a.levels_total, dim, a.trace_f + level);
+}
+
 // Last CTA: reduce the CTA records of this rank into the rank record and, on
 // a single rank, merge it into the annealer state (annealer.cpp:141-159).
 // Four records in flight per thread: the scan is L2-latency bound.
@@ -559,9 +607,12 @@ __device__ void reduce_block_records(RedShared<NT>& rs, const SaLevelArgs& a, in
         }
         *a.rank_rec = out;
         *a.ticket = 0u;
-        if (a.nranks == 1)
+        if (a.nranks == 1) {
             merge_level(a.state, &out, 1, a.n_chains, a.max_evals, a.levels_total, DIMF,
                         a.trace_f + level);
+        } else if (a.peer_boxes != nullptr) {
+            peer_exchange_and_merge(a, out, level, DIMF);
+        }
     }
 }
 

@@ -3,7 +3,11 @@ decomposition (chains split over ranks, per-level record all-gather, merge
 kernel) with the exchange over a gloo process group on the host.  Ranks may
 share one GPU.  Prints the reports of every workload as hex JSON (rank 0).
 
-  python tests/mr_engine_worker.py RANK WORLD PORT
+  python tests/mr_engine_worker.py RANK WORLD PORT [peer]
+
+With "peer" the T_I calibrators exchange their level records through the
+fused peer-memory path (sabr_ctx_enable_peer_exchange: CUDA IPC mailboxes,
+here between processes on one GPU) instead of the host all-gather.
 """
 import json
 import os
@@ -56,6 +60,7 @@ def workloads(eng):
 
 def main():
     rank, world, port = (int(x) for x in sys.argv[1:4])
+    peer = len(sys.argv) > 4 and sys.argv[4] == "peer"
     eng = pkg.Engine(0)
     if world > 1:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -67,6 +72,8 @@ def main():
             return b"".join(bytes(p.numpy().tobytes()) for p in parts)
 
         eng.init_host_exchange(rank, world, allgather)
+        if peer:
+            eng.enable_peer_exchange()
     out = workloads(eng)
     eng.close()
     if world > 1:

@@ -26,9 +26,10 @@ def free_port():
         return s.getsockname()[1]
 
 
-def run(world):
+def run(world, peer=False):
     port = free_port()
-    procs = [subprocess.Popen([sys.executable, WORKER, str(r), str(world), str(port)], cwd=ROOT,
+    extra = ["peer"] if peer else []
+    procs = [subprocess.Popen([sys.executable, WORKER, str(r), str(world), str(port)] + extra, cwd=ROOT,
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = [p.communicate(timeout=900) for p in procs]
     for p, (o, e) in zip(procs, outs):
@@ -41,5 +42,16 @@ def test_ranks_give_identical_reports():
     for world in (2, 3):
         many = run(world)
         assert many.keys() == one.keys()
+        for k in one:
+            assert many[k] == one[k], (world, k)
+
+
+def test_fused_peer_exchange_gives_identical_reports():
+    """The T_I level kernels' last CTAs exchange the level records through
+    CUDA-IPC mailboxes (peer memory) and merge in-kernel: same reports as one
+    rank (the other calibrators keep the host all-gather)."""
+    one = run(1)
+    for world in (2, 3):
+        many = run(world, peer=True)
         for k in one:
             assert many[k] == one[k], (world, k)
