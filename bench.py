@@ -159,13 +159,41 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SABR_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0, gloo for torch's collectives
+    # and the host all-gather as the engine transport, so the multi-rank code of this script runs
+    # on a single-GPU box; the numbers are not a scaling measurement
+    shared = os.environ.get("SABR_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
     eng = pkg.Engine(local, stream=stream.cuda_stream)
-    if world > 1:
+    if world > 1 and shared:
+        def allgather_gloo(send: bytes) -> bytes:
+            t = torch.frombuffer(bytearray(send), dtype=torch.uint8)
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t)
+            return b"".join(bytes(p.numpy().tobytes()) for p in parts)
+
+        eng.init_host_exchange(rank, world, allgather_gloo)
+        ok = torch.tensor([1], dtype=torch.int32)
+        try:
+            eng.enable_peer_exchange()
+        except pkg.SabrError:
+            ok.fill_(0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok) == 1:
+            transport = "fused peer-memory exchange (shared-GPU test mode)"
+        else:
+            eng.disable_peer_exchange()
+            transport = "host all-gather (shared-GPU test mode)"
+    elif world > 1:
         uid = torch.zeros(129, dtype=torch.uint8, device=dev)  # NCCL unique id + "ok" byte
         if rank == 0:
             try:
@@ -254,7 +282,7 @@ def run_ours(args):
     t_dev = sum(ev_times)
     t_wall = sum(walls)
     if world > 1:
-        tt = torch.tensor([t_dev, t_wall], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_dev, t_wall], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev, t_wall = tt.tolist()
     # evals reported by calibrate_* are global (all ranks' chains)
