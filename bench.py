@@ -387,9 +387,10 @@ def secondary(eng, torch, dev, stream):
 
     out = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for precision in ("fp64", "fp32"):
+    for precision, rng in (("fp64", "xoshiro"), ("fp32", "xoshiro"), ("fp64", "philox")):
         surf, fixed, sch, plan = c4_setup(levels=2)
         plan.precision = precision
+        plan.rng = rng
         small = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=32, t_min=1.5, seed=1)
         eng.calibrate_case2_T2(surf, None, small, plan, fixed)  # warm-up (jump tables, buffers)
         flush_l2(torch, dev)
@@ -402,9 +403,9 @@ def secondary(eng, torch, dev, stream):
         secs = e0.elapsed_time(e1) / 1e3
         steps_per_eval = 250
         ps = (rep.evals - 1) * plan.num_paths * steps_per_eval
-        key = "c4_mc_calibration" if precision == "fp64" else "c4_mc_calibration_fp32"
+        key = "c4_mc_calibration" + ("" if precision == "fp64" else "_fp32") + ("" if rng == "xoshiro" else "_philox")
         out[key] = {
-            "metric": f"MC SABR path-steps/s (calibrate_case2_T2 objective, C4, {precision})",
+            "metric": f"MC SABR path-steps/s (calibrate_case2_T2 objective, C4, {precision}, {rng} streams)",
             "unit": "path-steps/s", "value": ps / secs,
             "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
             "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,

@@ -407,7 +407,8 @@ SABR_HD void dyn_coeffs_case1(double rho0, double nu0, double a, double b, doubl
         const double x2 = SABR_MUL(xb, xb);
         const double c6 = SABR_DIV(6.0, SABR_MUL(x2, xb));
         // 6/(x^3) * (x*x/2 - x + 1 - e)
-        f1 = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_DIV(x2, 2.0), xb), 1.0), e));
+        // x*x/2 as a multiply by 0.5: halving is exact, so the bits equal the reference division
+        f1 = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), xb), 1.0), e));
         // 6/(x^3) * (2*(e-1) + x*(e+1))
         f2 = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(xb, SABR_ADD(e, 1.0))));
     }
