@@ -299,6 +299,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     int64_t launched = 0;
     auto* done_flag = static_cast<int64_t*>(ctx->pinned);
     for (int64_t level = 0; level < L; ++level) {
+        NvtxRange nvtx_level("sabr.level");
         if (a.n_local > 0) {
             timer.before();
             check_cuda(level_fn(a, level, temps[level]), "sa_level");
@@ -1157,6 +1158,7 @@ SABR_API sabr_status sabr_calibrate_static_T1(sabr_ctx* ctx, const sabr_surface*
                                               const sabr_fixed* fixed, sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.calibrate_static_T1");
         if (!schedule) fail(SABR_E_INVALID, "schedule is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         surface.validate();
@@ -1214,6 +1216,7 @@ SABR_API sabr_status sabr_calibrate_dynamic_case1_T1(sabr_ctx* ctx, const sabr_s
                                                      const sabr_fixed* fixed, sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.calibrate_dynamic_case1_T1");
         if (!schedule) fail(SABR_E_INVALID, "schedule is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         surface.validate();
@@ -1270,6 +1273,7 @@ SABR_API sabr_status sabr_calibrate_case2_T2(sabr_ctx* ctx, const sabr_surface* 
                                              sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.calibrate_case2_T2");
         if (!schedule || !plan) fail(SABR_E_INVALID, "schedule/plan is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         surface.validate();
@@ -1343,6 +1347,7 @@ SABR_API sabr_status sabr_calibrate_case2_formula(sabr_ctx* ctx, const sabr_surf
                                                   const sabr_fixed* fixed, sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.calibrate_case2_formula");
         if (!schedule) fail(SABR_E_INVALID, "schedule is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         surface.validate();
@@ -1413,6 +1418,7 @@ SABR_API sabr_status sabr_evaluate_case1(sabr_ctx* ctx, const sabr_surface* surf
                                          const double* p, sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.evaluate_case1");
         if (!p) fail(SABR_E_INVALID, "params is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         evaluate_case1_impl(ctx, surface, p).write(report);
@@ -1424,6 +1430,7 @@ SABR_API sabr_status sabr_evaluate_case2_prices(sabr_ctx* ctx, const sabr_surfac
                                                 sabr_report* report) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.evaluate_case2_prices");
         if (!p || !plan) fail(SABR_E_INVALID, "params/plan is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         evaluate_case2_impl(ctx, surface, p, *plan).write(report);
@@ -1435,6 +1442,7 @@ SABR_API sabr_status sabr_cost_batch(sabr_ctx* ctx, int32_t model, const sabr_su
                                      const sabr_plan* plan, double* cost) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.cost_batch");
         if (n < 0 || (n > 0 && (!params || !cost))) fail(SABR_E_INVALID, "params/cost is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         if (model == SABR_MODEL_STATIC) {
@@ -1489,6 +1497,7 @@ SABR_API sabr_status sabr_implied_vol_batch(sabr_ctx* ctx, int32_t model,
                                             const double* params, int64_t n, double* vols) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.implied_vol_batch");
         if (n < 0 || (n > 0 && (!params || !vols))) fail(SABR_E_INVALID, "params/vols is null");
         const HostSurface surface = HostSurface::from_abi(surface_in);
         if (model == SABR_MODEL_STATIC) {
@@ -1546,6 +1555,7 @@ SABR_API sabr_status sabr_mc_simulate_terminals(sabr_ctx* ctx, int32_t model, co
                                                 const sabr_plan* plan, double* terminals) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.mc_simulate_terminals");
         if (!plan || !terminals) fail(SABR_E_INVALID, "plan/terminals is null");
         validate_model(model, params);
         validate_plan(*plan);
@@ -1616,6 +1626,7 @@ SABR_API sabr_status sabr_mc_price_european_batch(sabr_ctx* ctx, int32_t model, 
                                                   double* std_error) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.mc_price_european_batch");
         if (!plan || m < 0 || (m > 0 && (!strikes || !value || !std_error)))
             fail(SABR_E_INVALID, "null argument");
         validate_model(model, params);
@@ -1639,6 +1650,7 @@ SABR_API sabr_status sabr_mc_price_cliquet(sabr_ctx* ctx, int32_t model, const d
                                            double* std_error) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.mc_price_cliquet");
         if (!plan || !value || !std_error || (n_resets > 0 && !reset_dates))
             fail(SABR_E_INVALID, "null argument");
         validate_model(model, params);
@@ -1751,6 +1763,7 @@ SABR_API sabr_status sabr_minimize_builtin(sabr_ctx* ctx, int32_t objective, int
                                            sabr_anneal_result* result) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.minimize_builtin");
         if (!schedule || !result || !result->best_point) fail(SABR_E_INVALID, "null argument");
         validate_schedule(*schedule);
         if (dim < 1 || dim > 4) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
@@ -1854,6 +1867,7 @@ SABR_API sabr_status sabr_black_scholes_call_batch(sabr_ctx* ctx, int64_t n, con
                                                    const double* vol, double* price) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.black_scholes_call_batch");
         if (n <= 0) return;
         bs_batch(ctx, n, {spot, strike, rate, dividend, maturity, vol}, price,
                  [&](const std::vector<const double*>& d, double* o, int32_t* st) {
@@ -1868,6 +1882,7 @@ SABR_API sabr_status sabr_implied_vol_from_price_batch(sabr_ctx* ctx, int64_t n,
                                                        const double* maturity, double* vol) {
     return guarded([&] {
         CtxLock l(ctx);
+        NvtxRange nvtx("sabr.implied_vol_from_price_batch");
         if (n <= 0) return;
         bs_batch(ctx, n, {price, spot, strike, rate, dividend, maturity}, vol,
                  [&](const std::vector<const double*>& d, double* o, int32_t* st) {

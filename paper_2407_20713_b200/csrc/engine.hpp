@@ -10,6 +10,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "host_common.hpp"
 #include "kernels.hpp"
 #include "kernels_mc.hpp"
@@ -46,6 +48,15 @@ struct sabr_ctx {
 };
 
 namespace sabr_gpu {
+
+// NVTX range (nsys / ncu timelines): the C-ABI entry points, each temperature
+// level and each T_II step.  Header-only NVTX v3: no cost without a tool.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void* dev_buf(sabr_ctx* ctx, const std::string& key, size_t bytes);
 void check_cuda(cudaError_t e, const char* what);

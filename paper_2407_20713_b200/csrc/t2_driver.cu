@@ -188,6 +188,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
         ta.temp = temps[level];
         check_cuda(launch_t2_level_init(chains, a.state, ta, ctx->stream), "t2_level_init");
         for (int step = 0; step < sch.chain_length; ++step) {
+            NvtxRange nvtx_step("sabr.t2_step");
             check_cuda(launch_t2_propose(chains, a.state, ta, alpha0, beta, active, ctx->stream), "t2_propose");
             for (int32_t c0 = 0; c0 < n_local; c0 += chunk) {
                 const int32_t nc = std::min(chunk, n_local - c0);
