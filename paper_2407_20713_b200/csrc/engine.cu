@@ -1118,7 +1118,19 @@ SABR_API sabr_status sabr_ctx_enable_peer_exchange(sabr_ctx* ctx) {
         ctx->peer_boxes = upload(ctx, "peer_boxes", ptrs);
         ctx->peer_error = static_cast<int*>(dev_buf(ctx, "peer_error", sizeof(int)));
         check_cuda(cudaMemsetAsync(ctx->peer_error, 0, sizeof(int), ctx->stream), "memset");
+        // handshake: every rank's peer stores must arrive in every mailbox
+        // before the level kernels rely on them
+        const unsigned long long magic = 0x5AB200C0FFEE0000ull + static_cast<unsigned long long>(ctx->rank);
+        check_cuda(launch_peer_hello(ctx->peer_boxes, ctx->nranks, ctx->rank, magic, ctx->stream), "peer hello");
         sync(ctx);
+        allgather(ctx, dsend, drecv, sizeof(h));  // a barrier over the transport
+        sync(ctx);
+        std::vector<unsigned long long> hello(kMaxPeerRanks);
+        check_cuda(cudaMemcpy(hello.data(), box->hello, sizeof(unsigned long long) * kMaxPeerRanks,
+                              cudaMemcpyDeviceToHost), "D2H hello");
+        for (int r = 0; r < ctx->nranks; ++r)
+            if (hello[r] != 0x5AB200C0FFEE0000ull + static_cast<unsigned long long>(r))
+                fail(SABR_E_NCCL, "peer exchange: a peer's stores did not reach this rank's mailbox");
         ctx->peer_box = box;
         ctx->peer = true;
     });

@@ -53,7 +53,13 @@ constexpr int kMaxPeerRanks = 16;
 struct PeerMailbox {
     sabr_level_record rec[2][kMaxPeerRanks];
     unsigned long long epoch[2][kMaxPeerRanks];
+    unsigned long long hello[kMaxPeerRanks];  // handshake at enable time
 };
+
+// Handshake of sabr_ctx_enable_peer_exchange: write `magic` into slot
+// [my_rank] of every rank's mailbox (peer stores), fenced system-wide.
+cudaError_t launch_peer_hello(PeerMailbox* const* boxes, int nranks, int my_rank, unsigned long long magic,
+                              cudaStream_t s);
 
 struct SaLevelArgs {
     double lo[SABR_MAX_DIM];

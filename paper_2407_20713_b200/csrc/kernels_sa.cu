@@ -1326,6 +1326,19 @@ cudaError_t launch_sa_start(int kind, const SurfaceView& sv, const SaLevelArgs& 
 #undef CALL
 }
 
+namespace {
+__global__ void peer_hello_kernel(PeerMailbox* const* boxes, int nranks, int my_rank, unsigned long long magic) {
+    for (int r = 0; r < nranks; ++r) atomicExch(&boxes[r]->hello[my_rank], magic);
+    __threadfence_system();
+}
+}  // namespace
+
+cudaError_t launch_peer_hello(PeerMailbox* const* boxes, int nranks, int my_rank, unsigned long long magic,
+                              cudaStream_t s) {
+    peer_hello_kernel<<<1, 1, 0, s>>>(boxes, nranks, my_rank, magic);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sa_merge(const SaLevelArgs& a, const sabr_level_record* recs, int64_t level,
                             cudaStream_t s) {
     sa_merge_kernel<<<1, 1, 0, s>>>(a, recs, level);
