@@ -38,8 +38,12 @@ __global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_con
     int64_t idx = blockIdx.x;
     const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
     idx /= P.tile_count;
-    const int s = static_cast<int>(idx % P.n_slices);
-    const int g = static_cast<int>(idx / P.n_slices);
+    // slice-major over candidate groups, longest slices first (slice_order:
+    // slice indices by descending step count), so the longest blocks start in
+    // the first waves and the launch ends on short ones
+    const int g = static_cast<int>(idx % P.n_groups);
+    const int sr = static_cast<int>(idx / P.n_groups);
+    const int s = P.slice_order != nullptr ? P.slice_order[sr] : sr;
     const McSlice sl = P.slices[s];
     const int c0 = g * CB;
     const int mq = sl.q_end - sl.q_begin;
@@ -216,8 +220,12 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
     int64_t idx = blockIdx.x;
     const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
     idx /= P.tile_count;
-    const int s = static_cast<int>(idx % P.n_slices);
-    const int g = static_cast<int>(idx / P.n_slices);
+    // slice-major over candidate groups, longest slices first (slice_order:
+    // slice indices by descending step count), so the longest blocks start in
+    // the first waves and the launch ends on short ones
+    const int g = static_cast<int>(idx % P.n_groups);
+    const int sr = static_cast<int>(idx / P.n_groups);
+    const int s = P.slice_order != nullptr ? P.slice_order[sr] : sr;
     const McSlice sl = P.slices[s];
     const int c0 = g * CB;
     const int mq = sl.q_end - sl.q_begin;
@@ -542,6 +550,7 @@ cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
         q.tile_count = q.n_tiles;
     }
     const int n_groups = (q.n_cand + CB - 1) / CB;
+    q.n_groups = n_groups;
     const int64_t blocks = static_cast<int64_t>(q.tile_count) * q.n_slices * n_groups;
     if (blocks <= 0) return cudaSuccess;
     k<<<static_cast<unsigned>(blocks), kMcThreads, smem, s>>>(q);

@@ -34,6 +34,8 @@ struct McParams {
     int32_t n_tiles;        // path tiles per (candidate, slice)
     int32_t tile_begin;     // this launch simulates tiles [tile_begin, tile_begin + tile_count)
     int32_t tile_count;     // (<= 0: all n_tiles); T_II path sharding over ranks
+    int32_t n_groups;       // candidate groups of the launch (set by launch_mc_tiles)
+    const int32_t* slice_order;  // [n_slices] block order of the slices (null: 0, 1, ...)
     int32_t ppt;            // paths per thread (consecutive, same RNG block)
     int32_t rng;            // sabr_rng
     int64_t total_steps;    // row length of coef / hdt

@@ -117,6 +117,13 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     P.hdt = upload(ctx, "t2_hdt", job.hdt);
     P.strikes = upload(ctx, "t2_strikes", surface.K);
     P.jump = upload(ctx, "t2_jump", jump);
+    {  // MC blocks of the longest slices first (C5: 62..1250 steps per slice)
+        std::vector<int32_t> order(ns);
+        for (size_t i = 0; i < ns; ++i) order[i] = static_cast<int32_t>(i);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t x, int32_t y) { return job.slices[x].n_steps > job.slices[y].n_steps; });
+        P.slice_order = upload(ctx, "t2_slice_order", order);
+    }
     P.exptab = exp_table_device(ctx);
     P.logtab = log_table_device(ctx);
     P.sctab = sincos_table_device(ctx);
