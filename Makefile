@@ -13,8 +13,11 @@ LIB      := paper_2407_20713_b200/lib/libsabr_b200.so
 CU_SRCS  := $(SRC_DIR)/kernels_sa.cu $(SRC_DIR)/kernels_mc.cu $(SRC_DIR)/engine.cu \
             $(SRC_DIR)/t2_driver.cu $(SRC_DIR)/peak.cu $(SRC_DIR)/kernels_c2f.cu $(SRC_DIR)/kernels_bs.cu
 CPP_SRCS := $(SRC_DIR)/xoshiro_jump.cpp
+# host-only C++ (binary128 arithmetic, which nvcc's front end does not take)
+HOST_SRCS := $(SRC_DIR)/slice_qr.cpp
 OBJS     := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(CU_SRCS)) \
-            $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/%.o,$(CPP_SRCS))
+            $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/%.o,$(CPP_SRCS)) \
+            $(patsubst $(SRC_DIR)/%.cpp,$(OBJ_DIR)/host_%.o,$(HOST_SRCS))
 HDRS     := $(wildcard $(SRC_DIR)/*.hpp $(SRC_DIR)/*.cuh) include/sabr_b200.h
 
 .PHONY: all lib oracle clean
@@ -30,6 +33,10 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ_DIR)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(OBJ_DIR)/host_%.o: $(SRC_DIR)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(HOSTCXX) -std=c++17 -O2 -fPIC -fvisibility=hidden -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))

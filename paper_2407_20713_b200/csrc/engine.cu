@@ -14,6 +14,7 @@
 #include "device_common.cuh"
 #include "engine.hpp"
 #include "kernels_c2f.hpp"
+#include "slice_qr.hpp"
 #include "xoshiro_jump.hpp"
 
 #include <functional>
@@ -752,10 +753,13 @@ SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& 
                       const std::vector<double>* market) {
     const int ns = static_cast<int>(s.n());
     const int nq = static_cast<int>(s.total_quotes());
-    // layout: quotes (16-byte aligned records) first, then T, ln f (hi, lo)
-    std::vector<double> d(4 * static_cast<size_t>(nq) + 3 * ns);
+    // layout: quotes (16-byte aligned records) first, then the slices' QR
+    // factors (slice_qr.hpp), then T, ln f (hi, lo)
+    const size_t qr_off = 4 * static_cast<size_t>(nq);
+    std::vector<double> d(qr_off + static_cast<size_t>(kQrStride) * ns + 3 * ns);
     std::vector<int32_t> qoff(ns + 1);
-    double* sd = d.data() + 4 * static_cast<size_t>(nq);
+    double* sd = d.data() + qr_off + static_cast<size_t>(kQrStride) * ns;
+    std::vector<double> lms, mkts;
     for (int i = 0; i < ns; ++i) {
         const double f = s.forward(i);
         const double lf = std::log(f);
@@ -773,6 +777,14 @@ SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& 
             q[2] = m;
             q[3] = 1.0 / m;
         }
+        lms.clear();
+        mkts.clear();
+        for (int64_t j = s.off[i]; j < s.off[i + 1]; ++j) {
+            lms.push_back(d[4 * j]);
+            mkts.push_back(d[4 * j + 2]);
+        }
+        slice_qr_factor(lms.data(), mkts.data(), static_cast<int64_t>(lms.size()),
+                        d.data() + qr_off + static_cast<size_t>(kQrStride) * i);
     }
     qoff[ns] = nq;
     double* dd = upload(ctx, key + "_d", d);
@@ -781,7 +793,8 @@ SurfaceView make_view(sabr_ctx* ctx, const std::string& key, const HostSurface& 
     v.n_slices = ns;
     v.n_quotes = nq;
     v.quotes = dd;
-    v.T = dd + 4 * static_cast<size_t>(nq);
+    v.qr = dd + qr_off;
+    v.T = dd + qr_off + static_cast<size_t>(kQrStride) * ns;
     v.lnf_hi = v.T + ns;
     v.lnf_lo = v.T + 2 * ns;
     v.qoff = dq;

@@ -20,6 +20,9 @@ struct SurfaceView {
     // [n_quotes] x {lm = ln(K/f) (std::log(strike/forward), the reference
     // expression, evaluated on the host), lm*lm, market value, 1/market}
     const double* quotes;
+    // [n_slices][kQrStride]: each slice's cost as a 4x4 quadratic form
+    // (slice_qr.hpp), nullptr when the view has none
+    const double* qr;
     const double2* exptab;  // [128] exp_tab table (device_common.cuh), staged per CTA
     double max_abs_lnf;     // max_i |ln f_i| (host-side bound for the unsaturated exp)
 };

@@ -14,10 +14,13 @@
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
+#include <string>
+#include <type_traits>
 #include <math_constants.h>
 
 #include "device_common.cuh"
 #include "kernels.hpp"
+#include "slice_qr.hpp"
 
 namespace sabr_gpu {
 
@@ -370,14 +373,134 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const P
     }
 }
 
-// Objective grid of the SA / cost kernels: the padded SoA grid when it fits
-// in shared memory, else the AoS grid read through L1.
-template <bool SMEM>
-using ObjGrid = std::conditional_t<SMEM, PGrid, Grid>;
+// ------------------------------------------- factored slice cost (QR) ---
+// The default objective of the SA and cost kernels (slice_qr.hpp): a slice's
+// sum of squared relative errors is ||R (C0, A1, A2, -1)||^2 with the slice's
+// 4x4 factor R, computed on the host in binary128.  Nine FP64 instructions per
+// slice replace the four per quote; the grid a CTA stages is kQrStride + 3
+// doubles per slice.
+struct QGrid {
+    int ns;
+    const double* T;
+    const double* lnf_hi;
+    const double* lnf_lo;
+    const double* R;  // [ns][kQrStride], 16-byte aligned
+    const double2* tab;
+};
 
-template <bool SMEM>
-__device__ __forceinline__ ObjGrid<SMEM> stage_obj(const SurfaceView& sv, unsigned char* smem) {
-    if constexpr (SMEM) return stage_pgrid(sv, smem);
+__host__ __device__ inline size_t qstage_bytes(int ns) {
+    return sizeof(double) * static_cast<size_t>(kQrStride + 3) * ns;
+}
+
+__device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
+    const int ns = sv.n_slices;
+    double* R = reinterpret_cast<double*>(smem);
+    double* d = R + kQrStride * ns;
+    for (int k = threadIdx.x; k < kQrStride * ns; k += blockDim.x) R[k] = sv.qr[k];
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        d[i] = sv.T[i];
+        d[ns + i] = sv.lnf_hi[i];
+        d[2 * ns + i] = sv.lnf_lo[i];
+    }
+    __syncthreads();
+    QGrid g;
+    g.ns = ns;
+    g.R = R;
+    g.T = d;
+    g.lnf_hi = d + ns;
+    g.lnf_lo = d + 2 * ns;
+    g.tab = nullptr;
+    return g;
+}
+
+// One slice's factor in registers (the static objective's only slice).
+struct QrFactor {
+    double r00, r01, r02, r03, r11, r12, r13, r22, r23, r33sq;
+};
+
+__device__ __forceinline__ QrFactor load_qr(const double* R) {
+    const double2* p = reinterpret_cast<const double2*>(R);
+    const double2 a = p[0], b = p[1], c = p[2], d = p[3], e = p[4];
+    return QrFactor{a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
+}
+
+__device__ __forceinline__ double qr_cost(const QuadTerms& t, const QrFactor& f) {
+    const double u0 = fma(f.r02, t.a2, fma(f.r01, t.a1, fma(f.r00, t.c0, -f.r03)));
+    const double u1 = fma(f.r12, t.a2, fma(f.r11, t.a1, -f.r13));
+    const double u2 = fma(f.r22, t.a2, -f.r23);
+    return fma(u0, u0, fma(u1, u1, fma(u2, u2, f.r33sq)));
+}
+
+__device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
+    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
+    return qr_cost(quad_terms(static_terms(v[0], v[1], v[2], v[3], pw, g.T[0])), load_qr(g.R));
+}
+
+__device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
+    double sum = 0.0;
+    const double omb = 1.0 - v[1];
+    for (int i = 0; i < g.ns; ++i) {
+        const double T = g.T[i];
+        double n1, n2, e1, e2;
+        dyn_coeffs_case1(v[2], v[3], v[4], v[5], T, n1, n2, e1, e2);
+        const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+        sum += qr_cost(quad_terms(dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, T)), load_qr(g.R + kQrStride * i));
+    }
+    return sum;
+}
+
+struct QrSlice {  // the static objective's slice, hoisted into registers
+    double lnf_hi, lnf_lo, T;
+    QrFactor f;
+};
+
+__device__ __forceinline__ QrSlice qr_slice(const QGrid& g) {
+    return QrSlice{g.lnf_hi[0], g.lnf_lo[0], g.T[0], load_qr(g.R)};
+}
+
+template <int C, int DIMF, bool FAST>
+__device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const QrSlice& sl,
+                                              const double2* tab, double (&out)[C]) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const double pw = pow_fwd<!FAST>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
+        out[c] = qr_cost(quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, sl.T)), sl.f);
+    }
+}
+
+template <int C, int DIMF>
+__device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const QGrid& g,
+                                             double (&out)[C]) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[c] = 0.0;
+    for (int i = 0; i < g.ns; ++i) {
+        const double T = g.T[i];
+        const QrFactor f = load_qr(g.R + kQrStride * i);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double n1, n2, e1, e2;
+            dyn_coeffs_case1(v[c][2], v[c][3], v[c][4], v[c][5], T, n1, n2, e1, e2);
+            const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            out[c] += qr_cost(quad_terms(dynamic_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T)), f);
+        }
+    }
+}
+
+// Objective grid of the SA / cost kernels (GK): kGridQR the factored slices
+// (default), kGridQuads the padded per-quote grid in shared memory
+// (SABR_SA_COST=quotes), kGridL1 the AoS per-quote grid read through L1 (a
+// per-quote grid too large for shared memory).
+constexpr int kGridL1 = 0;
+constexpr int kGridQuads = 1;
+constexpr int kGridQR = 2;
+
+template <int GK>
+using ObjGrid = std::conditional_t<GK == kGridQR, QGrid, std::conditional_t<GK == kGridQuads, PGrid, Grid>>;
+
+template <int GK>
+__device__ __forceinline__ ObjGrid<GK> stage_obj(const SurfaceView& sv, unsigned char* smem) {
+    if constexpr (GK == kGridQR) return stage_qgrid(sv, smem);
+    else if constexpr (GK == kGridQuads) return stage_pgrid(sv, smem);
     else return stage_grid<false>(sv, smem);
 }
 
@@ -648,7 +771,7 @@ __device__ __forceinline__ double propose_coord_fast(double x, double step_scale
 // ALLFREE (the FAST variant): every coordinate is searched (no mask test),
 // one reflection always lands in the box (propose_coord_fast) and every
 // forward has |ln f| <= 700 (unsaturated exp in pow_fwd) - see sa_fast_path.
-template <int KIND, int DIMF, bool ALLFREE, bool SMEM>
+template <int KIND, int DIMF, bool ALLFREE, int GK>
 __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
     sa_level_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                     const int64_t level, const double temp, const double inv_temp) {
@@ -665,8 +788,8 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
     if (st->done) return;  // early-stopped run (max_evals): uniform exit
 
     stage_exp(sv, tab_s);
-    ObjGrid<SMEM> g{};
-    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<SMEM>(sv, smem);
+    ObjGrid<GK> g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
 
@@ -754,24 +877,24 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
     reduce_block_records<NT, DIMF>(rs, a, level);
 }
 
-// The same level with kCpt chains per thread (model objectives, grid in
-// shared memory, no predicate): the chains of a thread step in lockstep and
-// share the quote loads, the loop control and the constants, and their
-// independent dependency chains interleave (ILP).  A CTA of kPairThreads
-// threads covers kPairThreads * kCpt = kLevelThreads chains (thread t owns
-// chains t and t + kPairThreads of the CTA's range), so the per-CTA records
-// are those of sa_level_kernel.  Each chain's arithmetic is that of
-// sa_level_kernel: the two kernels produce identical trajectories.
-constexpr int kCpt = 2;
-constexpr int kPairThreads = kLevelThreads / kCpt;
-constexpr int kPairMinCtas = 11;  // 1e5 chains: 1563 CTAs of 32 threads in one wave
+// The same level with C chains per thread (model objectives, grid in shared
+// memory, no predicate), with a branch-free Metropolis step and programmatic
+// dependent launch.  With C = 2 the chains of a thread step in lockstep and
+// share the grid loads, the loop control and the constants, and their
+// independent dependency chains interleave (ILP).  A CTA of kLevelThreads / C
+// threads covers kLevelThreads chains (thread t owns chains t, t + NT, ...
+// of the CTA's range), so the per-CTA records are those of sa_level_kernel.
+// Each chain's arithmetic is that of sa_level_kernel: the kernels produce
+// identical trajectories.  C = 2 (default): 32-thread CTAs; C = 1
+// (SABR_SA_CPT=1, factored grid only): 64-thread CTAs.  1e5 chains: 1563
+// CTAs, 11 per SM, in one wave either way.
+constexpr int kPairMinCtas = 11;
 
-template <int KIND, int DIMF, bool ALLFREE>
-__global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
+__global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
-    constexpr int NT = kPairThreads;
-    constexpr int C = kCpt;
+    constexpr int NT = kLevelThreads / C;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
     __shared__ sabr_level_record rec;
@@ -786,7 +909,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
     // previous level is read before pdl_wait().
     pdl_trigger();
     stage_exp(sv, tab_s);
-    PGrid g = stage_pgrid(sv, smem);
+    ObjGrid<GK> g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
 
@@ -822,8 +945,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinCtas)
         double step_scale[DIMF];
 #pragma unroll
         for (int i = 0; i < DIMF; ++i) step_scale[i] = __dmul_rn(a.range[i], scale);
-        StaticSlice sl{};
-        if constexpr (KIND == OBJ_STATIC) sl = static_slice(g);
+        std::conditional_t<GK == kGridQR, QrSlice, StaticSlice> sl{};
+        if constexpr (KIND == OBJ_STATIC) {
+            if constexpr (GK == kGridQR) sl = qr_slice(g);
+            else sl = static_slice(g);
+        }
         for (int step = 0; step < steps; ++step) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
@@ -910,13 +1036,13 @@ __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* re
                 a.trace_f + level);
 }
 
-template <int KIND, int DIMF, bool SMEM>
+template <int KIND, int DIMF, int GK>
 __global__ void sa_start_kernel(const __grid_constant__ SurfaceView sv, const SaLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 tab_s[kExpTableSize];
     stage_exp(sv, tab_s);
-    ObjGrid<SMEM> g{};
-    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<SMEM>(sv, smem);
+    ObjGrid<GK> g{};
+    if constexpr (KIND != OBJ_BUILTIN) g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
     if (threadIdx.x != 0) return;
@@ -929,14 +1055,14 @@ __global__ void sa_start_kernel(const __grid_constant__ SurfaceView sv, const Sa
 }
 
 // The SA objective on a batch of full parameter vectors (same code path).
-template <int KIND, int DIMF, bool SMEM>
+template <int KIND, int DIMF, int GK>
 __global__ void __launch_bounds__(kThreads)
     cost_batch_kernel(const __grid_constant__ SurfaceView sv, const double* __restrict__ params,
                       const int64_t n, double* __restrict__ cost) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 tab_s[kExpTableSize];
     stage_exp(sv, tab_s);
-    ObjGrid<SMEM> g = stage_obj<SMEM>(sv, smem);
+    ObjGrid<GK> g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
@@ -1181,25 +1307,56 @@ cudaError_t set_smem(K kernel, size_t bytes) {
 // the padded grid staged in shared memory, or (too large) the AoS grid read
 // through L1.  (Kernel-parameter/constant-bank grids were tried: sm_100a FP64
 // instructions take no constant-bank operands, so they only add registers.)
+// SABR_SA_COST=quotes selects the per-quote objectives (A/B checks).
+bool qr_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SABR_SA_COST");
+        return !(e && std::string(e) == "quotes");
+    }();
+    return on;
+}
+
+// The objective grid of a model view: the factored slices when the view has
+// them, else the padded per-quote grid in shared memory, else the AoS grid
+// through L1.  *smem = the dynamic shared memory it stages.
+int grid_kind(const SurfaceView& sv, size_t* smem) {
+    if (sv.qr != nullptr && qr_enabled() && qstage_bytes(sv.n_slices) <= kSmemStageLimit) {
+        *smem = qstage_bytes(sv.n_slices);
+        return kGridQR;
+    }
+    int use = 0;
+    *smem = smem_for(sv, &use, true);
+    return use ? kGridQuads : kGridL1;
+}
+
+template <int GK>
+using GridTag = std::integral_constant<int, GK>;
+
 template <int KIND, class Pick, class Body>
 cudaError_t dispatch_grid(const SurfaceView& sv, Pick&& pick, Body&& body) {
     if constexpr (KIND == OBJ_BUILTIN) {
-        return body(pick(std::true_type{}), size_t(0));
+        return body(pick(GridTag<kGridQuads>{}), size_t(0));
     } else {
-        int use = 0;
-        const size_t smem = smem_for(sv, &use, true);
-        if (use) return body(pick(std::true_type{}), smem);
-        return body(pick(std::false_type{}), size_t(0));
+        size_t smem = 0;
+        switch (grid_kind(sv, &smem)) {
+            case kGridQR: return body(pick(GridTag<kGridQR>{}), smem);
+            case kGridQuads: return body(pick(GridTag<kGridQuads>{}), smem);
+            default: return body(pick(GridTag<kGridL1>{}), size_t(0));
+        }
     }
 }
 
-// SABR_SA_CPT=1 selects the one-chain-per-thread level kernel (A/B checks).
-bool multi_chain_enabled() {
-    static const bool on = [] {
+// Chains per thread of the model-objective level kernel: SABR_SA_CPT=1 or 2
+// (default 2); SABR_SA_CPT=0 selects the general one-chain kernel
+// sa_level_kernel (A/B checks).
+int chains_per_thread() {
+    static const int c = [] {
         const char* e = std::getenv("SABR_SA_CPT");
-        return !(e && std::atoi(e) == 1);
+        if (!e) return 2;
+        const int v = std::atoi(e);
+        return v == 0 || v == 1 ? v : 2;
     }();
-    return on;
+    return c;
 }
 
 // SABR_SA_PDL=0 launches the level kernels without programmatic dependent launch.
@@ -1225,15 +1382,24 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
         return cudaGetLastError();
     };
     if constexpr (KIND != OBJ_BUILTIN) {
-        int use = 0;
-        const size_t smem = smem_for(sv, &use, true);
-        if (use && multi_chain_enabled()) {
-            auto k = all_free ? sa_level_multi_kernel<KIND, DIMF, true> : sa_level_multi_kernel<KIND, DIMF, false>;
+        size_t smem = 0;
+        const int gk = grid_kind(sv, &smem);
+        const int cpt = chains_per_thread();
+        if ((gk == kGridQR && cpt > 0) || (gk == kGridQuads && cpt == 2)) {
+            using K = decltype(&sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 2>);
+            const K kq2[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2>,
+                              sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 2>};
+            const K kq1[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 1>,
+                              sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 1>};
+            const K kp2[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQuads, 2>,
+                              sa_level_multi_kernel<KIND, DIMF, true, kGridQuads, 2>};
+            const K k = (gk == kGridQR ? (cpt == 1 ? kq1 : kq2) : kp2)[all_free ? 1 : 0];
+            const unsigned threads = static_cast<unsigned>(kLevelThreads / cpt);
             cudaError_t e = set_smem(k, smem);
             if (e != cudaSuccess) return e;
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(grid);
-            cfg.blockDim = dim3(kPairThreads);
+            cfg.blockDim = dim3(threads);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
             cudaLaunchAttribute attr[1];

@@ -52,6 +52,25 @@ def test_static_cost_parity(engine, ref, request, fixture):
         assert err < TOL, f"slice {sl}: {err:.3e}"
 
 
+def test_static_cost_parity_small_and_large_slices(engine, ref):
+    """The factored slice cost (slice_qr.hpp) on slices of 1, 2, 3 quotes
+    (rank-deficient factors: R has zero rows), 4 (square), and 600 quotes."""
+    rng = np.random.default_rng(7)
+    slices = []
+    for n in (1, 2, 3, 4, 600):
+        K = np.sort(rng.uniform(0.6, 1.5, n))
+        v = rng.uniform(0.08, 0.6, n)
+        slices.append(pkg.VolSlice(0.25 + 0.5 * len(slices), 0.01, 0.002,
+                                   [pkg.VolQuote(float(k), float(x)) for k, x in zip(K, v)]))
+    surface = pkg.VolSurface(1.0, slices)
+    P = static_vectors(4_000, 44)
+    for sl in range(len(slices)):
+        got = engine.cost_batch(pkg.MODEL_STATIC, surface, P, slice=sl)
+        want = ref.cost_static(surface, sl, P)
+        err = mixed_err(got, want)
+        assert err < TOL, f"slice {sl}: {err:.3e}"
+
+
 @pytest.mark.parametrize("fixture", ["eq_surface", "fx_surface"])
 def test_case1_cost_parity(engine, ref, orc, request, fixture):
     from oracles import cost_sensitivity

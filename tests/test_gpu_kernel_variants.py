@@ -1,8 +1,11 @@
 """The T_I level kernel variants must produce bit-identical annealer
-trajectories: one chain per thread vs kCpt chains per thread sharing the quote
-loads (SABR_SA_CPT=1 selects the former), and the FAST propose/exp path
-(one reflection, unsaturated exp; kernels_sa.cu propose_coord_fast) vs the
-general one (SABR_SA_FAST=0).  The switches are read once per process, so
+trajectories: two chains per thread (default), one chain per thread in the
+same kernel (SABR_SA_CPT=1) and the general one-chain kernel (SABR_SA_CPT=0);
+the FAST propose/exp path (one reflection, unsaturated exp; kernels_sa.cu
+propose_coord_fast) vs the general one (SABR_SA_FAST=0).  The factored slice
+cost (slice_qr.hpp, default) and the per-quote sum (SABR_SA_COST=quotes)
+round differently, so between them the decisions (evals, trace length) must
+agree and the values to 1e-12.  The switches are read once per process, so
 each variant runs in its own subprocess."""
 import json
 import os
@@ -42,26 +45,51 @@ print(json.dumps(out))
 """
 
 
-def run_variant(cpt, fast=None):
+def run_variant(cpt, fast=None, cost=None):
     env = dict(os.environ)
-    env.pop("SABR_SA_CPT", None)
-    env.pop("SABR_SA_FAST", None)
+    for k in ("SABR_SA_CPT", "SABR_SA_FAST", "SABR_SA_COST"):
+        env.pop(k, None)
     if cpt is not None:
         env["SABR_SA_CPT"] = str(cpt)
     if fast is not None:
         env["SABR_SA_FAST"] = str(fast)
+    if cost is not None:
+        env["SABR_SA_COST"] = cost
     p = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     return json.loads(p.stdout.strip().splitlines()[-1])
 
 
-def test_multi_chain_kernel_matches_single_chain_kernel():
-    multi = run_variant(None)
-    single = run_variant(1)
-    assert multi.keys() == single.keys()
-    for k in multi:
-        assert multi[k] == single[k], k
+@pytest.mark.parametrize("cost", [None, "quotes"])
+def test_multi_chain_kernel_matches_single_chain_kernels(cost):
+    multi = run_variant(None, cost=cost)
+    for cpt in ((1, 0) if cost is None else (0,)):
+        single = run_variant(cpt, cost=cost)
+        assert multi.keys() == single.keys()
+        for k in multi:
+            assert multi[k] == single[k], (cpt, k)
+
+
+def _close(a, b, rel):
+    a, b = float.fromhex(a), float.fromhex(b)
+    return abs(a - b) <= rel * max(abs(a), abs(b), 1e-300)
+
+
+def test_factored_cost_matches_per_quote_cost():
+    qr = run_variant(None)
+    quotes = run_variant(None, cost="quotes")
+    for k in qr:
+        a, b = qr[k], quotes[k]
+        assert _close(a[0], b[0], 1e-12), k
+        tr_a, tr_b = a[-1], b[-1]
+        assert len(tr_a) == len(tr_b), k
+        assert all(_close(x, y, 1e-12) for x, y in zip(tr_a, tr_b)), k
+        if isinstance(a[1], dict):
+            assert a[2] == b[2], k  # evals
+            assert all(_close(a[1][p], b[1][p], 1e-9) for p in a[1]), k
+        else:
+            assert a[1] == b[1], k
 
 
 def test_fast_propose_matches_general_propose():
