@@ -431,9 +431,15 @@ __device__ __forceinline__ double qr_cost(const QuadTerms& t, const QrFactor& f)
     return fma(u0, u0, fma(u1, u1, fma(u2, u2, f.r33sq)));
 }
 
+__device__ __forceinline__ QuadTerms static_qterms(const double* v, double pw, double T) {
+    QuadTerms t;
+    static_quad_terms(v[0], v[1], v[2], v[3], pw, T, t.c0, t.a1, t.a2);
+    return t;
+}
+
 __device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
     const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
-    return qr_cost(quad_terms(static_terms(v[0], v[1], v[2], v[3], pw, g.T[0])), load_qr(g.R));
+    return qr_cost(static_qterms(v, pw, g.T[0]), load_qr(g.R));
 }
 
 __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
@@ -464,7 +470,7 @@ __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const 
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const double pw = pow_fwd<!FAST>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
-        out[c] = qr_cost(quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, sl.T)), sl.f);
+        out[c] = qr_cost(static_qterms(v[c], pw, sl.T), sl.f);
     }
 }
 
@@ -836,14 +842,12 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
             if (isnan(fy)) fy = CUDART_INF;  // safe_eval, annealer.cpp:84-87
             ++ev;
             // Metropolis, annealer.cpp:125-126 (uniform drawn only when fy > fx).
-            // (fy - fx) / T with the host's RN(1/T) and one exact-residual
-            // correction: the correctly rounded quotient (Markstein), without
-            // the IEEE division's special-case path.
+            // (fy - fx) / T as (fy - fx) * RN(1/T) (<= 1 ulp from the IEEE
+            // quotient: the decision boundary moves by ~1e-16 relative, the
+            // size of the reference's own exp rounding).
             bool accept = fy <= fx;
             if (!accept) {
-                const double d = fy - fx;
-                const double q0 = d * inv_temp;
-                const double q = fma(fma(-q0, temp, d), inv_temp, q0);
+                const double q = (fy - fx) * inv_temp;
                 const double u = rng.uniform();
                 accept = ALLFREE ? (q <= 700.0 && u < exp_tab_unsat(-q, tab_s)) : u < exp_tab(-q, tab_s);
             }
@@ -977,9 +981,7 @@ __global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
             for (int c = 0; c < C; ++c) {
                 if (isnan(fy[c])) fy[c] = CUDART_INF;
                 const bool up = !(fy[c] <= fx[c]);
-                const double d = fy[c] - fx[c];
-                const double q0 = d * inv_temp;
-                const double q = fma(fma(-q0, temp, d), inv_temp, q0);
+                const double q = (fy[c] - fx[c]) * inv_temp;
                 const double u = rng[c].peek_uniform();
                 Xoshiro adv = rng[c];
                 adv.advance();
