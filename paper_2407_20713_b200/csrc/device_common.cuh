@@ -525,6 +525,107 @@ SABR_HD void static_quad_terms(double alpha, double beta, double nu, double rho,
     c0 = fma(inv, B * T, inv);
 }
 
+// dynamic_terms (below) folded into the terms of the factored cost like
+// static_quad_terms, with q = (1-beta)/omega and p = q - eta1:
+//     A1/omega = -p/2
+//     A2/omega = (1-beta) q / 12 + p / 4 + (4 nu1^2 + 3 (eta2^2 - 3 eta1^2)) omega / 24
+//     B        = q^2/24 + beta eta1 / (4 omega) + (2 nu2^2 - 3 eta2^2) / 24
+//     C0       = 1/omega + (1/omega) B T
+SABR_HD void dynamic_quad_terms(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double alpha,
+                                double beta, double pw, double T, double& c0, double& a1, double& a2) {
+    const double omb = 1.0 - beta;
+    const double r = fast_rcp(alpha * pw);
+    const double inv = alpha * (alpha * r);
+    const double omega = pw * (pw * r);
+    const double q = omb * inv;
+    const double p = q - eta1;
+    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
+    a1 = -0.5 * p;
+    a2 = fma(k * (1.0 / 24.0), omega, fma(0.25, p, (omb * q) * (1.0 / 12.0)));
+    const double B = fma(q * (1.0 / 24.0), q, fma((0.25 * beta) * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0)));
+    c0 = fma(inv, B * T, inv);
+}
+
+#ifdef __CUDACC__
+// The Taylor tables of series_nu1 .. series_eta2 as one 64-double block
+// (4 series x 16, two trailing zeros each), for a shared-memory copy: FP64
+// instructions take no immediate or constant-bank operands, so unrolled
+// Horner loops over compile-time tables rematerialise every coefficient with
+// two uniform moves per use; from shared memory one LDS.128 brings two.
+constexpr int kSeriesStride = 16;
+__device__ __forceinline__ double series_coef(int fn, int i) {
+    constexpr double c[4][kSeriesStride] = {
+        {1.0, -1.0 / 4, 1.0 / 20, -1.0 / 120, 1.0 / 840, -1.0 / 6720, 1.0 / 60480, -1.0 / 604800,
+         1.0 / 6652800, -1.0 / 79833600, 1.0 / 1037836800, -1.0 / 14529715200.0, 1.0 / 217945728000.0,
+         -1.0 / 3487131648000.0, 0.0, 0.0},
+        {1.0, -1.0 / 2, 3.0 / 20, -1.0 / 30, 1.0 / 168, -1.0 / 1120, 1.0 / 8640, -1.0 / 75600,
+         1.0 / 739200, -1.0 / 7983360, 1.0 / 94348800, -1.0 / 1210809600, 1.0 / 16765056000.0,
+         -1.0 / 249080832000.0, 0.0, 0.0},
+        {1.0, -1.0 / 3, 1.0 / 12, -1.0 / 60, 1.0 / 360, -1.0 / 2520, 1.0 / 20160, -1.0 / 181440,
+         1.0 / 1814400, -1.0 / 19958400, 1.0 / 239500800, -1.0 / 3113510400.0, 1.0 / 43589145600.0,
+         -1.0 / 653837184000.0, 0.0, 0.0},
+        {1.0, -3.0 / 5, 7.0 / 30, -1.0 / 14, 31.0 / 1680, -1.0 / 240, 127.0 / 151200, -17.0 / 110880,
+         73.0 / 2851200, -31.0 / 7862400, 2047.0 / 3632428800.0, -1.0 / 13305600, 8191.0 / 871782912000.0,
+         -5461.0 / 4940103168000.0, 0.0, 0.0}};
+    return c[fn][i];
+}
+
+// Horner over the shared-memory copy (ser: 4 x kSeriesStride doubles).
+__device__ __forceinline__ double horner_s(const double* __restrict__ ser, int fn, double x) {
+    const double2* c = reinterpret_cast<const double2*>(ser + fn * kSeriesStride);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 6; k >= 0; --k) {
+        const double2 cc = c[k];
+        acc = fma(fma(acc, x, cc.y), x, cc.x);
+    }
+    return acc;
+}
+
+// dyn_coeffs_case1 for the factored objectives: the series from shared
+// memory (horner_s), the reciprocals as MUFU + Newton (<= 1 ulp from the
+// reference's quotients; they scale the cancelling brackets, they are not
+// inside them) and exp by table (exp_tab, ~0.5 ulp).  The brackets keep the
+// reference's operation order and roundings.
+__device__ __forceinline__ void dyn_coeffs_case1_fast(double rho0, double nu0, double a, double b, double T,
+                                                      const double* __restrict__ ser,
+                                                      const double2* __restrict__ tab, double& nu1_sq,
+                                                      double& nu2_sq, double& eta1, double& eta2_sq) {
+    constexpr double kXSwitch = 0.25;  // analytics.cpp:21
+    const double xb = SABR_MUL(SABR_MUL(2.0, b), T);
+    const double xab = SABR_MUL(SABR_ADD(a, b), T);
+    const double nn = SABR_MUL(nu0, nu0);
+    const double nr = SABR_MUL(nu0, rho0);
+    double f1, f2, g1, g2;
+    if (xb < kXSwitch) {
+        f1 = horner_s(ser, 0, xb);
+        f2 = horner_s(ser, 1, xb);
+    } else {
+        const double e = exp_tab(-xb, tab);
+        const double x2 = SABR_MUL(xb, xb);
+        const double c6 = 6.0 * fast_rcp(SABR_MUL(x2, xb));
+        f1 = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), xb), 1.0), e));
+        f2 = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(xb, SABR_ADD(e, 1.0))));
+    }
+    if (xab < kXSwitch) {
+        g1 = horner_s(ser, 2, xab);
+        g2 = horner_s(ser, 3, xab);
+    } else {
+        const double e = exp_tab(-xab, tab);
+        const double x2 = SABR_MUL(xab, xab);
+        g1 = SABR_MUL(2.0 * fast_rcp(x2), SABR_SUB(e, SABR_SUB(1.0, xab)));
+        const double x4 = SABR_MUL(SABR_MUL(x2, xab), xab);
+        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
+                                     SABR_MUL(SABR_MUL(2.0, xab), SABR_SUB(xab, 3.0)));
+        g2 = SABR_MUL(3.0 * fast_rcp(x4), poly);
+    }
+    nu1_sq = SABR_MUL(nn, f1);
+    nu2_sq = SABR_MUL(nn, f2);
+    eta1 = SABR_MUL(nr, g1);
+    eta2_sq = SABR_MUL(SABR_MUL(nr, nr), g2);
+}
+#endif
+
 // dynamic_implied_vol, analytics.cpp:291-312 (strike-independent part).
 SABR_HD SmileTerms dynamic_terms(double nu1_sq, double nu2_sq, double eta1, double eta2_sq,
                                  double alpha, double beta, double pw, double T) {

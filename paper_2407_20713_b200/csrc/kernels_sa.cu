@@ -384,18 +384,22 @@ struct QGrid {
     const double* T;
     const double* lnf_hi;
     const double* lnf_lo;
-    const double* R;  // [ns][kQrStride], 16-byte aligned
+    const double* R;    // [ns][kQrStride], 16-byte aligned
+    const double* ser;  // [4][kSeriesStride] Case I series tables (horner_s)
     const double2* tab;
 };
 
 __host__ __device__ inline size_t qstage_bytes(int ns) {
-    return sizeof(double) * static_cast<size_t>(kQrStride + 3) * ns;
+    return sizeof(double) * (4 * kSeriesStride + static_cast<size_t>(kQrStride + 3) * ns);
 }
 
 __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
     const int ns = sv.n_slices;
-    double* R = reinterpret_cast<double*>(smem);
+    double* ser = reinterpret_cast<double*>(smem);
+    double* R = ser + 4 * kSeriesStride;
     double* d = R + kQrStride * ns;
+    for (int k = threadIdx.x; k < 4 * kSeriesStride; k += blockDim.x)
+        ser[k] = series_coef(k / kSeriesStride, k % kSeriesStride);
     for (int k = threadIdx.x; k < kQrStride * ns; k += blockDim.x) R[k] = sv.qr[k];
     for (int i = threadIdx.x; i < ns; i += blockDim.x) {
         d[i] = sv.T[i];
@@ -406,6 +410,7 @@ __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
     QGrid g;
     g.ns = ns;
     g.R = R;
+    g.ser = ser;
     g.T = d;
     g.lnf_hi = d + ns;
     g.lnf_lo = d + 2 * ns;
@@ -448,9 +453,11 @@ __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
     for (int i = 0; i < g.ns; ++i) {
         const double T = g.T[i];
         double n1, n2, e1, e2;
-        dyn_coeffs_case1(v[2], v[3], v[4], v[5], T, n1, n2, e1, e2);
+        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, g.ser, g.tab, n1, n2, e1, e2);
         const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
-        sum += qr_cost(quad_terms(dynamic_terms(n1, n2, e1, e2, v[0], v[1], pw, T)), load_qr(g.R + kQrStride * i));
+        QuadTerms t;
+        dynamic_quad_terms(n1, n2, e1, e2, v[0], v[1], pw, T, t.c0, t.a1, t.a2);
+        sum += qr_cost(t, load_qr(g.R + kQrStride * i));
     }
     return sum;
 }
@@ -485,9 +492,11 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             double n1, n2, e1, e2;
-            dyn_coeffs_case1(v[c][2], v[c][3], v[c][4], v[c][5], T, n1, n2, e1, e2);
+            dyn_coeffs_case1_fast(v[c][2], v[c][3], v[c][4], v[c][5], T, g.ser, g.tab, n1, n2, e1, e2);
             const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
-            out[c] += qr_cost(quad_terms(dynamic_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T)), f);
+            QuadTerms t;
+            dynamic_quad_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
+            out[c] += qr_cost(t, f);
         }
     }
 }
