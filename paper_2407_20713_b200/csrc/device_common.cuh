@@ -582,6 +582,63 @@ __device__ __forceinline__ double horner_s(const double* __restrict__ ser, int f
     return acc;
 }
 
+// The two functionals of one argument (f_nu1/f_nu2 at x = 2bT: PAIR 0;
+// f_eta1/f_eta2 at x = (a+b)T: PAIR 1), analytics.cpp:47-67, in the
+// arithmetic of dyn_coeffs_case1_fast.
+template <int PAIR>
+__device__ __forceinline__ void case1_series_pair(double x, const double* __restrict__ ser, double& f,
+                                                  double& g) {
+    f = horner_s(ser, 2 * PAIR, x);
+    g = horner_s(ser, 2 * PAIR + 1, x);
+}
+
+template <int PAIR>
+__device__ __forceinline__ void case1_closed_pair(double x, const double2* __restrict__ tab, double& f,
+                                                  double& g) {
+    const double e = exp_tab(-x, tab);
+    const double x2 = SABR_MUL(x, x);
+    if constexpr (PAIR == 0) {
+        const double c6 = 6.0 * fast_rcp(SABR_MUL(x2, x));
+        f = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), x), 1.0), e));
+        g = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(x, SABR_ADD(e, 1.0))));
+    } else {
+        f = SABR_MUL(2.0 * fast_rcp(x2), SABR_SUB(e, SABR_SUB(1.0, x)));
+        const double x4 = SABR_MUL(SABR_MUL(x2, x), x);
+        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
+                                     SABR_MUL(SABR_MUL(2.0, x), SABR_SUB(x, 3.0)));
+        g = SABR_MUL(3.0 * fast_rcp(x4), poly);
+    }
+}
+
+// One functional pair for C chains: when every chain of the thread takes the
+// same branch (the rule late in a schedule, when the chains cluster), their
+// evaluations share one branch body and interleave (C-fold ILP); mixed
+// threads evaluate chain by chain.  Per-chain results do not depend on C.
+template <int PAIR, int C>
+__device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
+                                             const double2* __restrict__ tab, double (&f)[C], double (&g)[C]) {
+    constexpr double kXSwitch = 0.25;  // analytics.cpp:21
+    bool all_series = true, all_closed = true;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        all_series &= x[c] < kXSwitch;
+        all_closed &= !(x[c] < kXSwitch);
+    }
+    if (all_series) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+    } else if (all_closed) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) case1_closed_pair<PAIR>(x[c], tab, f[c], g[c]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if (x[c] < kXSwitch) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+            else case1_closed_pair<PAIR>(x[c], tab, f[c], g[c]);
+        }
+    }
+}
+
 // dyn_coeffs_case1 for the factored objectives: the series from shared
 // memory (horner_s), the reciprocals as MUFU + Newton (<= 1 ulp from the
 // reference's quotients; they scale the cancelling brackets, they are not
@@ -591,38 +648,17 @@ __device__ __forceinline__ void dyn_coeffs_case1_fast(double rho0, double nu0, d
                                                       const double* __restrict__ ser,
                                                       const double2* __restrict__ tab, double& nu1_sq,
                                                       double& nu2_sq, double& eta1, double& eta2_sq) {
-    constexpr double kXSwitch = 0.25;  // analytics.cpp:21
-    const double xb = SABR_MUL(SABR_MUL(2.0, b), T);
-    const double xab = SABR_MUL(SABR_ADD(a, b), T);
+    const double xb[1] = {SABR_MUL(SABR_MUL(2.0, b), T)};
+    const double xab[1] = {SABR_MUL(SABR_ADD(a, b), T)};
     const double nn = SABR_MUL(nu0, nu0);
     const double nr = SABR_MUL(nu0, rho0);
-    double f1, f2, g1, g2;
-    if (xb < kXSwitch) {
-        f1 = horner_s(ser, 0, xb);
-        f2 = horner_s(ser, 1, xb);
-    } else {
-        const double e = exp_tab(-xb, tab);
-        const double x2 = SABR_MUL(xb, xb);
-        const double c6 = 6.0 * fast_rcp(SABR_MUL(x2, xb));
-        f1 = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), xb), 1.0), e));
-        f2 = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(xb, SABR_ADD(e, 1.0))));
-    }
-    if (xab < kXSwitch) {
-        g1 = horner_s(ser, 2, xab);
-        g2 = horner_s(ser, 3, xab);
-    } else {
-        const double e = exp_tab(-xab, tab);
-        const double x2 = SABR_MUL(xab, xab);
-        g1 = SABR_MUL(2.0 * fast_rcp(x2), SABR_SUB(e, SABR_SUB(1.0, xab)));
-        const double x4 = SABR_MUL(SABR_MUL(x2, xab), xab);
-        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
-                                     SABR_MUL(SABR_MUL(2.0, xab), SABR_SUB(xab, 3.0)));
-        g2 = SABR_MUL(3.0 * fast_rcp(x4), poly);
-    }
-    nu1_sq = SABR_MUL(nn, f1);
-    nu2_sq = SABR_MUL(nn, f2);
-    eta1 = SABR_MUL(nr, g1);
-    eta2_sq = SABR_MUL(SABR_MUL(nr, nr), g2);
+    double f1[1], f2[1], g1[1], g2[1];
+    case1_pair_n<0, 1>(xb, ser, tab, f1, f2);
+    case1_pair_n<1, 1>(xab, ser, tab, g1, g2);
+    nu1_sq = SABR_MUL(nn, f1[0]);
+    nu2_sq = SABR_MUL(nn, f2[0]);
+    eta1 = SABR_MUL(nr, g1[0]);
+    eta2_sq = SABR_MUL(SABR_MUL(nr, nr), g2[0]);
 }
 #endif
 

@@ -489,13 +489,22 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
     for (int i = 0; i < g.ns; ++i) {
         const double T = g.T[i];
         const QrFactor f = load_qr(g.R + kQrStride * i);
+        // dyn_coeffs_case1_fast for the C chains, branch bodies shared
+        double xb[C], xab[C], f1[C], f2[C], g1[C], g2[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            double n1, n2, e1, e2;
-            dyn_coeffs_case1_fast(v[c][2], v[c][3], v[c][4], v[c][5], T, g.ser, g.tab, n1, n2, e1, e2);
+            xb[c] = SABR_MUL(SABR_MUL(2.0, v[c][5]), T);
+            xab[c] = SABR_MUL(SABR_ADD(v[c][4], v[c][5]), T);
+        }
+        case1_pair_n<0, C>(xb, g.ser, g.tab, f1, f2);
+        case1_pair_n<1, C>(xab, g.ser, g.tab, g1, g2);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const double nn = SABR_MUL(v[c][3], v[c][3]), nr = SABR_MUL(v[c][3], v[c][2]);
             const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
             QuadTerms t;
-            dynamic_quad_terms(n1, n2, e1, e2, v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
+            dynamic_quad_terms(SABR_MUL(nn, f1[c]), SABR_MUL(nn, f2[c]), SABR_MUL(nr, g1[c]),
+                               SABR_MUL(SABR_MUL(nr, nr), g2[c]), v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
             out[c] += qr_cost(t, f);
         }
     }

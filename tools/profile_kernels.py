@@ -5,6 +5,8 @@
   python tools/profile_kernels.py t2      # C4 T_II: one level, 3 SA steps (MC tile kernel)
   python tools/profile_kernels.py mc      # price_european_batch, 2^20 paths (C4 pricing)
   python tools/profile_kernels.py c5      # C5 T_II: full Case II, 20x30 surface, 512 chains, 1 step
+  python tools/profile_kernels.py sa_full     # the whole C2 schedule on slice 0 (412 levels)
+  python tools/profile_kernels.py case1_full  # the whole C3 schedule (412 levels, beta = 1)
 """
 import os
 import sys
@@ -27,6 +29,13 @@ def main(mode):
         s = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8,
                                   t_min=2.0 * 0.96 ** 2 * 0.999, max_evals=10 ** 12, seed=1)
         r = eng.calibrate_dynamic_case1_T1(fx, None, s, {"beta": 1.0})
+    elif mode in ("sa_full", "case1_full"):
+        s = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8,
+                                  t_min=1e-7, max_evals=10 ** 12, seed=1)
+        if mode == "sa_full":
+            r = eng.calibrate_static_T1(fx, 0, None, s, None)
+        else:
+            r = eng.calibrate_dynamic_case1_T1(fx, None, s, {"beta": 1.0})
     elif mode == "t2":
         surf = pkg.VolSurface(eq.spot, [eq.slices[2]])
         fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
