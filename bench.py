@@ -337,12 +337,17 @@ def run_ours(args):
         "gpu_launches": int(launches_tot),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "sa_level_multi_kernel<OBJ_STATIC,4,ALLFREE> (2 chains per thread)",
+                     "kernel": "sa_level_multi_kernel<OBJ_STATIC,4,ALLFREE,QR> (2 chains per thread, factored slice cost)",
                      "avg_launch_ms": avg_launch_s * 1e3, "launches": klaunch_tot,
                      "flops_per_eval": per_eval["flops"], "flops_source": per_eval["source"],
                      "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
-                     "fp64_pipe": pipe},
+                     "fp64_pipe": pipe,
+                     # SURVEY 8(d)'s per-quote form (4-quote-independent terms hoisted,
+                     # 2 divisions per quote): ~1180 FP64 instructions per C2 eval; the
+                     # factored slice cost (slice_qr.hpp) executes fp64_instr_per_eval
+                     "survey_8d_fp64_instr_per_eval": 1180,
+                     "fp64_instr_per_eval": per_eval.get("instr")},
         "clocks": clocks.summary(),
     }
     if sec:
@@ -373,7 +378,7 @@ def fp64_flops_per_eval():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return {"flops": d["c2_flops_per_eval"], "source": d["source"],
+        return {"flops": d["c2_flops_per_eval"], "source": d["source"], "instr": d.get("c2_fp64_instr_per_eval"),
                 "dram_bytes_per_launch": d.get("c2_dram_bytes_per_launch"),
                 "pipe_instr": d.get("c2_fp64_pipe_instr_per_eval")}
     # ~1180 FP64-pipe instructions per eval at m = 19 (upper bound,

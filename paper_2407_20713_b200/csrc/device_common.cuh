@@ -553,22 +553,19 @@ SABR_HD void dynamic_quad_terms(double nu1_sq, double nu2_sq, double eta1, doubl
 // Horner loops over compile-time tables rematerialise every coefficient with
 // two uniform moves per use; from shared memory one LDS.128 brings two.
 constexpr int kSeriesStride = 16;
-__device__ __forceinline__ double series_coef(int fn, int i) {
-    constexpr double c[4][kSeriesStride] = {
-        {1.0, -1.0 / 4, 1.0 / 20, -1.0 / 120, 1.0 / 840, -1.0 / 6720, 1.0 / 60480, -1.0 / 604800,
-         1.0 / 6652800, -1.0 / 79833600, 1.0 / 1037836800, -1.0 / 14529715200.0, 1.0 / 217945728000.0,
-         -1.0 / 3487131648000.0, 0.0, 0.0},
-        {1.0, -1.0 / 2, 3.0 / 20, -1.0 / 30, 1.0 / 168, -1.0 / 1120, 1.0 / 8640, -1.0 / 75600,
-         1.0 / 739200, -1.0 / 7983360, 1.0 / 94348800, -1.0 / 1210809600, 1.0 / 16765056000.0,
-         -1.0 / 249080832000.0, 0.0, 0.0},
-        {1.0, -1.0 / 3, 1.0 / 12, -1.0 / 60, 1.0 / 360, -1.0 / 2520, 1.0 / 20160, -1.0 / 181440,
-         1.0 / 1814400, -1.0 / 19958400, 1.0 / 239500800, -1.0 / 3113510400.0, 1.0 / 43589145600.0,
-         -1.0 / 653837184000.0, 0.0, 0.0},
-        {1.0, -3.0 / 5, 7.0 / 30, -1.0 / 14, 31.0 / 1680, -1.0 / 240, 127.0 / 151200, -17.0 / 110880,
-         73.0 / 2851200, -31.0 / 7862400, 2047.0 / 3632428800.0, -1.0 / 13305600, 8191.0 / 871782912000.0,
-         -5461.0 / 4940103168000.0, 0.0, 0.0}};
-    return c[fn][i];
-}
+static __constant__ double kCase1Series[4 * kSeriesStride] = {
+    1.0, -1.0 / 4, 1.0 / 20, -1.0 / 120, 1.0 / 840, -1.0 / 6720, 1.0 / 60480, -1.0 / 604800,
+    1.0 / 6652800, -1.0 / 79833600, 1.0 / 1037836800, -1.0 / 14529715200.0, 1.0 / 217945728000.0,
+    -1.0 / 3487131648000.0, 0.0, 0.0,
+    1.0, -1.0 / 2, 3.0 / 20, -1.0 / 30, 1.0 / 168, -1.0 / 1120, 1.0 / 8640, -1.0 / 75600,
+    1.0 / 739200, -1.0 / 7983360, 1.0 / 94348800, -1.0 / 1210809600, 1.0 / 16765056000.0,
+    -1.0 / 249080832000.0, 0.0, 0.0,
+    1.0, -1.0 / 3, 1.0 / 12, -1.0 / 60, 1.0 / 360, -1.0 / 2520, 1.0 / 20160, -1.0 / 181440,
+    1.0 / 1814400, -1.0 / 19958400, 1.0 / 239500800, -1.0 / 3113510400.0, 1.0 / 43589145600.0,
+    -1.0 / 653837184000.0, 0.0, 0.0,
+    1.0, -3.0 / 5, 7.0 / 30, -1.0 / 14, 31.0 / 1680, -1.0 / 240, 127.0 / 151200, -17.0 / 110880,
+    73.0 / 2851200, -31.0 / 7862400, 2047.0 / 3632428800.0, -1.0 / 13305600, 8191.0 / 871782912000.0,
+    -5461.0 / 4940103168000.0, 0.0, 0.0};
 
 // Horner over the shared-memory copy (ser: 4 x kSeriesStride doubles).
 __device__ __forceinline__ double horner_s(const double* __restrict__ ser, int fn, double x) {

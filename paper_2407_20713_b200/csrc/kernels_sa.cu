@@ -398,8 +398,7 @@ __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
     double* ser = reinterpret_cast<double*>(smem);
     double* R = ser + 4 * kSeriesStride;
     double* d = R + kQrStride * ns;
-    for (int k = threadIdx.x; k < 4 * kSeriesStride; k += blockDim.x)
-        ser[k] = series_coef(k / kSeriesStride, k % kSeriesStride);
+    for (int k = threadIdx.x; k < 4 * kSeriesStride; k += blockDim.x) ser[k] = kCase1Series[k];
     for (int k = threadIdx.x; k < kQrStride * ns; k += blockDim.x) R[k] = sv.qr[k];
     for (int i = threadIdx.x; i < ns; i += blockDim.x) {
         d[i] = sv.T[i];
