@@ -480,9 +480,12 @@ __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const 
     }
 }
 
+// pw_fixed: when beta is not searched, f_i^(1-beta) per slice, computed once
+// per CTA with the same pow_fwd (so the values are the ones each chain would
+// compute); nullptr when beta is free.
 template <int C, int DIMF>
 __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const QGrid& g,
-                                             double (&out)[C]) {
+                                             double (&out)[C], const double* pw_fixed = nullptr) {
 #pragma unroll
     for (int c = 0; c < C; ++c) out[c] = 0.0;
     for (int i = 0; i < g.ns; ++i) {
@@ -500,7 +503,7 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const double nn = SABR_MUL(v[c][3], v[c][3]), nr = SABR_MUL(v[c][3], v[c][2]);
-            const double pw = pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            const double pw = pw_fixed ? pw_fixed[i] : pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
             QuadTerms t;
             dynamic_quad_terms(SABR_MUL(nn, f1[c]), SABR_MUL(nn, f2[c]), SABR_MUL(nr, g1[c]),
                                SABR_MUL(SABR_MUL(nr, nr), g2[c]), v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
@@ -910,6 +913,7 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
 // (SABR_SA_CPT=1, factored grid only): 64-thread CTAs.  1e5 chains: 1563
 // CTAs, 11 per SM, in one wave either way.
 constexpr int kPairMinCtas = 11;
+constexpr int kMaxPwSlices = 64;
 
 template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
 __global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
@@ -947,6 +951,17 @@ __global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
     }
     pdl_wait();
     if (st->done) return;  // early-stopped run (max_evals): uniform exit
+    // Case I with beta not searched: f_i^(1-beta) is one value per slice
+    __shared__ double pw_s[kMaxPwSlices];
+    const double* pw_fixed = nullptr;
+    if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
+        if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {
+            const double omb = 1.0 - st->incumbent[1];
+            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            __syncthreads();
+            pw_fixed = pw_s;
+        }
+    }
     double x[C][DIMF], y[C][DIMF], fx[C], bv[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -988,6 +1003,7 @@ __global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
             }
             double fy[C];
             if constexpr (KIND == OBJ_STATIC) static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
+            else if constexpr (GK == kGridQR) case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
             else case1_cost_n<C, DIMF>(y, g, fy);
             // Metropolis (annealer.cpp:125-126) without a branch, so the
             // chains' exp chains interleave: exp(-(fy - fx)/T) and the

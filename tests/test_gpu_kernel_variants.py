@@ -41,6 +41,10 @@ s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.8, chain_length=40, workers=129, t_
 r = eng.calibrate_dynamic_case1_T1(fx, None, s3, None, trace=True)
 out["case1"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
                 [f.hex() for _, f in r.temperature_trace]]
+# beta not searched: the two-chain kernel takes f^(1-beta) per CTA, the others per chain
+r = eng.calibrate_dynamic_case1_T1(eq, None, s3, {"beta": 0.7}, trace=True)
+out["case1_beta_fixed"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                           [f.hex() for _, f in r.temperature_trace]]
 print(json.dumps(out))
 """
 
