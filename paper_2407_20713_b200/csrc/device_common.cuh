@@ -101,16 +101,18 @@ struct Xoshiro {
         advance();
         return result;
     }
+    // (n >> 11) * 2^-53 is computed as (n & ~0x7ff) * 2^-64: the masked value
+    // has at most 53 significant bits, so its conversion is exact and the
+    // products are the same doubles (one LOP3 instead of a 64-bit shift).
+    static SABR_HD double top53(uint64_t n) { return static_cast<double>(n & ~0x7ffull); }
     // the uniform() that the next draw would return, without drawing it
-    SABR_HD double peek_uniform() const {
-        return static_cast<double>((rotl64c<23>(s0 + s3) + s0) >> 11) * 0x1.0p-53;
-    }
+    SABR_HD double peek_uniform() const { return top53(rotl64c<23>(s0 + s3) + s0) * 0x1.0p-64; }
     // uniform(), rng.hpp:42: (next() >> 11) * 2^-53 (exact conversion)
-    SABR_HD double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    SABR_HD double uniform() { return top53(next()) * 0x1.0p-64; }
     // 2*uniform() - 1 (annealer.cpp:66) in one exact FMA: (n >> 11) * 2^-52
     // is exact and the difference with 1 is representable, so this equals
     // the reference's RN(RN(2u) - 1) bit for bit.
-    SABR_HD double sym() { return fma(static_cast<double>(next() >> 11), 0x1.0p-52, -1.0); }
+    SABR_HD double sym() { return fma(top53(next()), 0x1.0p-63, -1.0); }
 
     // state <- M^k state, where x^k mod P(x) = sum_i poly_i x^i (256 bits,
     // host-computed; see xoshiro_jump.cpp).  Branch-free masked accumulate.
@@ -166,8 +168,8 @@ SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, dou
     philox4x32_10(static_cast<uint32_t>(path), static_cast<uint32_t>(path >> 32), step, 0u, seed, x);
     const uint64_t a = (static_cast<uint64_t>(x[0]) << 32) | x[1];
     const uint64_t b = (static_cast<uint64_t>(x[2]) << 32) | x[3];
-    ua = static_cast<double>(a >> 11) * 0x1.0p-53;
-    ub = static_cast<double>(b >> 11) * 0x1.0p-53;
+    ua = Xoshiro::top53(a) * 0x1.0p-64;
+    ub = Xoshiro::top53(b) * 0x1.0p-64;
 }
 
 // ------------------------------------------------------------ fast exp ---
