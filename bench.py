@@ -305,6 +305,16 @@ def run_ours(args):
         pipe = {"instr_per_eval": per_eval["pipe_instr"], "achieved_Tinstr_per_s": pa,
                 "peak_Tinstr_per_s": peak / 2, "frac": pa / (peak / 2)}
 
+    # and as issue-slot occupancy: warp instructions per eval (ncu) against one
+    # instruction per cycle per scheduler (148 SMs x 4) at the sampled SM clock
+    issue = None
+    clk = clocks.summary().get("sm_mhz") if hasattr(clocks, "summary") else None
+    if per_eval.get("warp_instr") and clk:
+        ia = evals_per_launch * per_eval["warp_instr"] / avg_launch_s
+        ip = 148 * 4 * clk * 1e6
+        issue = {"warp_instr_per_eval": per_eval["warp_instr"], "achieved_warp_instr_per_s": ia,
+                 "peak_warp_instr_per_s": ip, "frac": ia / ip}
+
     sec = {}
     if rank == 0 and world == 1 and not args.no_secondary:
         sec = secondary(eng, torch, dev, stream)
@@ -343,6 +353,7 @@ def run_ours(args):
                      "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
                      "fp64_pipe": pipe,
+                     "issue": issue,
                      # SURVEY 8(d)'s per-quote form (4-quote-independent terms hoisted,
                      # 2 divisions per quote): ~1180 FP64 instructions per C2 eval; the
                      # factored slice cost (slice_qr.hpp) executes fp64_instr_per_eval
@@ -380,7 +391,8 @@ def fp64_flops_per_eval():
             d = json.load(f)
         return {"flops": d["c2_flops_per_eval"], "source": d["source"], "instr": d.get("c2_fp64_instr_per_eval"),
                 "dram_bytes_per_launch": d.get("c2_dram_bytes_per_launch"),
-                "pipe_instr": d.get("c2_fp64_pipe_instr_per_eval")}
+                "pipe_instr": d.get("c2_fp64_pipe_instr_per_eval"),
+                "warp_instr": d.get("c2_warp_instr_per_eval")}
     # ~1180 FP64-pipe instructions per eval at m = 19 (upper bound,
     # counts one FLOP per instruction)
     return {"flops": 1180.0, "source": "SURVEY.md 8(d) estimate (FP64-pipe instr, m=19)"}

@@ -19,9 +19,10 @@ def per(path, prefix, units, pick=-1):
     dadd = g["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
     dmul = g["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"]
     pipe = g.get("smsp__inst_executed_pipe_fp64.sum")  # warp instructions of the FP64 pipe
+    warp_inst = g.get("smsp__inst_executed.sum")
     return ((2 * dfma + dadd + dmul) / units, (dfma + dadd + dmul) / units,
             g["dram__bytes_read.sum"] + g["dram__bytes_write.sum"], g["gpu__time_duration.sum"],
-            None if pipe is None else 32 * pipe / units)
+            None if pipe is None else 32 * pipe / units, None if warp_inst is None else warp_inst / units)
 
 
 def main(tag, copy=("sa", "case1", "t2", "t2_cb4", "mc")):
@@ -34,6 +35,7 @@ def main(tag, copy=("sa", "case1", "t2", "t2_cb4", "mc")):
                    f"per unit, profiles/{tag}_ncu_metrics_*.csv (tools/profile_kernels.py)",
          "c2_flops_per_eval": sa[0], "c2_fp64_instr_per_eval": sa[1], "c2_dram_bytes_per_launch": sa[2],
          "c2_level_kernel_ns": sa[3], "c2_fp64_pipe_instr_per_eval": sa[4],
+         "c2_warp_instr_per_eval": sa[5],
          "c3_flops_per_eval": c1[0], "c3_fp64_instr_per_eval": c1[1], "c3_dram_bytes_per_launch": c1[2],
          "c3_level_kernel_ns": c1[3],
          "c4_flops_per_candidate_path_step": t2[0], "c4_fp64_instr_per_candidate_path_step": t2[1],
