@@ -32,7 +32,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <int CB>
-__global__ void __launch_bounds__(kMcThreads, 3) mc_tile_kernel(const __grid_constant__ McParams P) {
+__global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_constant__ McParams P) {
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
     int64_t idx = blockIdx.x;
