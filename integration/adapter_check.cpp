@@ -2,6 +2,8 @@
 // the adapter's sabr::b200::calibrate_* (B200 engine) on the same inputs and
 // prints one JSON line per case (doubles as hex) for tests/test_gpu_adapter.py.
 //   adapter_check <data dir>
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -87,6 +89,50 @@ int main(int argc, char** argv) {
     plan.seed = 1;
     emit("case2_T2", calibrate_case2_T2(one, {}, s4, plan, fixed), b200::calibrate_case2_T2(one, {}, s4, plan, fixed));
 
+    // the Monte Carlo operator (mc.hpp:66-84): same streams, prices to rounding
+    mc::SimulationPlan mp;
+    mp.num_paths = 1u << 16;
+    mp.seed = 3;
+    const std::vector<double> strikes{1900.0, 2100.0, 2257.37, 2400.0, 2700.0};
+    auto emit_prices = [&](const char* name, const std::vector<mc::PriceEstimate>& r,
+                           const std::vector<mc::PriceEstimate>& g) {
+        std::string a = "[", b = "[";
+        for (size_t j = 0; j < r.size(); ++j) {
+            a += "[" + hx(r[j].value) + ", " + hx(r[j].std_error) + "]" + (j + 1 < r.size() ? ", " : "");
+            b += "[" + hx(g[j].value) + ", " + hx(g[j].std_error) + "]" + (j + 1 < g.size() ? ", " : "");
+        }
+        std::printf("{\"case\": \"%s\", \"ref\": %s], \"b200\": %s]}\n", name, a.c_str(), b.c_str());
+    };
+    const StaticSabrParams sp{0.375162, 0.7, 0.331441, -0.6};
+    emit_prices("mc_static", mc::price_european_batch(mc::ModelDynamics::from_static(sp), 2257.37, strikes, 0.018196,
+                                                      0.034516, 0.495890, mp),
+                b200::price_european_batch(sp, 2257.37, strikes, 0.018196, 0.034516, 0.495890, mp));
+    const CaseIParams c1{0.3, 1.0, -0.4, 0.6, 1.5, 0.8};
+    emit_prices("mc_case1", mc::price_european_batch(mc::ModelDynamics::from_case1(c1), 2257.37, strikes, 0.018196,
+                                                     0.034516, 0.99, mp),
+                b200::price_european_batch(c1, 2257.37, strikes, 0.018196, 0.034516, 0.99, mp));
+    const CaseIIParams c2{0.3, 1.0, -0.4, 0.1, 0.05, 0.6, -0.1, 0.1, 1.0, 0.5, 1.0};
+    emit_prices("mc_case2", mc::price_european_batch(mc::ModelDynamics::from_case2(c2), 2257.37, strikes, 0.018196,
+                                                     0.034516, 1.0, mp),
+                b200::price_european_batch(c2, 2257.37, strikes, 0.018196, 0.034516, 1.0, mp));
+    {
+        mc::SimulationPlan tp = mp;
+        tp.num_paths = 10000;
+        tp.block_size = 1000;
+        const auto r = mc::simulate_terminals(mc::ModelDynamics::from_static(sp), 2300.0, sp.alpha, 0.75, tp);
+        const auto g = b200::simulate_terminals(sp, 2300.0, sp.alpha, 0.75, tp);
+        double worst = r.size() == g.size() ? 0.0 : 1.0;
+        for (size_t i = 0; i < std::min(r.size(), g.size()); ++i)
+            worst = std::max(worst, std::fabs(g[i] - r[i]) / std::fabs(r[i]));
+        std::printf("{\"case\": \"mc_terminals\", \"n\": %zu, \"max_rel\": %.3e}\n", g.size(), worst);
+    }
+    {
+        mc::CliquetSpec cs{-0.05, 0.05, 0.0, 0.2, {0.25, 0.5, 0.75, 1.0}};
+        const auto r = mc::price_cliquet(mc::ModelDynamics::from_static(sp), 2257.37, 0.018196, 0.034516, cs, mp);
+        const auto g = b200::price_cliquet(sp, 2257.37, 0.018196, 0.034516, cs, mp);
+        emit_prices("mc_cliquet", {r}, {g});
+    }
+
     // the reference's exception types come back through the adapter (test_calibration.cpp:212-225)
     const std::string r1 = kind([&] { calibrate_static_T1(eq, 9, {}, s1); });
     const std::string g1 = kind([&] { b200::calibrate_static_T1(eq, 9, {}, s1); });
@@ -94,7 +140,12 @@ int main(int argc, char** argv) {
     const std::string g2 = kind([&] { b200::calibrate_static_T1(eq, 0, {{"nu", {5.0, 0.01}}}, s1); });
     const std::string r3 = kind([&] { calibrate_static_T1(eq, 0, {}, s1, {{"gamma", 1.0}}); });
     const std::string g3 = kind([&] { b200::calibrate_static_T1(eq, 0, {}, s1, {{"gamma", 1.0}}); });
-    std::printf("{\"case\": \"errors\", \"ref\": [\"%s\", \"%s\", \"%s\"], \"b200\": [\"%s\", \"%s\", \"%s\"]}\n",
-                r1.c_str(), r2.c_str(), r3.c_str(), g1.c_str(), g2.c_str(), g3.c_str());
+    mc::SimulationPlan bad = mp;
+    bad.num_paths = 0;
+    const std::string r4 = kind([&] { mc::price_european_batch(mc::ModelDynamics::from_static(sp), 2257.37, strikes, 0.0, 0.0, 1.0, bad); });
+    const std::string g4 = kind([&] { b200::price_european_batch(sp, 2257.37, strikes, 0.0, 0.0, 1.0, bad); });
+    std::printf("{\"case\": \"errors\", \"ref\": [\"%s\", \"%s\", \"%s\", \"%s\"], "
+                "\"b200\": [\"%s\", \"%s\", \"%s\", \"%s\"]}\n",
+                r1.c_str(), r2.c_str(), r3.c_str(), r4.c_str(), g1.c_str(), g2.c_str(), g3.c_str(), g4.c_str());
     return 0;
 }

@@ -114,7 +114,84 @@ CalibrationReport run(const VolSurface& s, const BoundsOverrides& bounds, const 
     return out;
 }
 
+// Parameter structs -> (sabr_model, flat vector in the ABI's order).
+struct ModelArgs {
+    int32_t model;
+    std::vector<double> v;
+};
+ModelArgs model_args(const StaticSabrParams& p) { return {SABR_MODEL_STATIC, {p.alpha, p.beta, p.nu, p.rho}}; }
+ModelArgs model_args(const CaseIParams& p) {
+    return {SABR_MODEL_CASE1, {p.alpha, p.beta, p.rho0, p.nu0, p.a, p.b}};
+}
+ModelArgs model_args(const CaseIIParams& p) {
+    return {SABR_MODEL_CASE2,
+            {p.alpha, p.beta, p.rho0, p.q_rho, p.d_rho, p.nu0, p.q_nu, p.d_nu, p.a, p.b, p.horizon}};
+}
+
 }  // namespace
+
+template <class Params>
+std::vector<double> simulate_terminals(const Params& p, double forward0, double alpha0, double maturity,
+                                       const mc::SimulationPlan& plan) {
+    const ModelArgs m = model_args(p);
+    const sabr_plan pl = to_abi(plan);
+    std::vector<double> out(plan.num_paths);
+    if (sabr_status st = sabr_mc_simulate_terminals(context(), m.model, m.v.data(), forward0, alpha0, maturity,
+                                                    &pl, out.data()))
+        rethrow(st);
+    return out;
+}
+
+template <class Params>
+std::vector<mc::PriceEstimate> price_european_batch(const Params& p, double spot, const std::vector<double>& strikes,
+                                                    double rate, double dividend, double maturity,
+                                                    const mc::SimulationPlan& plan) {
+    const ModelArgs m = model_args(p);
+    const sabr_plan pl = to_abi(plan);
+    std::vector<double> value(strikes.size()), se(strikes.size());
+    if (sabr_status st = sabr_mc_price_european_batch(context(), m.model, m.v.data(), spot, strikes.data(),
+                                                      static_cast<int64_t>(strikes.size()), rate, dividend,
+                                                      maturity, &pl, value.data(), se.data()))
+        rethrow(st);
+    std::vector<mc::PriceEstimate> out;
+    for (size_t j = 0; j < strikes.size(); ++j) out.push_back({value[j], se[j], plan.num_paths});
+    return out;
+}
+
+template <class Params>
+mc::PriceEstimate price_european_call(const Params& p, double spot, double strike, double rate, double dividend,
+                                      double maturity, const mc::SimulationPlan& plan) {
+    return price_european_batch(p, spot, std::vector<double>{strike}, rate, dividend, maturity, plan)[0];
+}
+
+template <class Params>
+mc::PriceEstimate price_cliquet(const Params& p, double spot, double rate, double dividend,
+                                const mc::CliquetSpec& spec, const mc::SimulationPlan& plan) {
+    const ModelArgs m = model_args(p);
+    const sabr_plan pl = to_abi(plan);
+    double value = 0.0, se = 0.0;
+    if (sabr_status st = sabr_mc_price_cliquet(context(), m.model, m.v.data(), spot, rate, dividend,
+                                               spec.local_floor, spec.local_cap, spec.global_floor, spec.global_cap,
+                                               spec.reset_dates.data(), static_cast<int64_t>(spec.reset_dates.size()),
+                                               &pl, &value, &se))
+        rethrow(st);
+    return {value, se, plan.num_paths};
+}
+
+#define SABR_B200_MC(P)                                                                                        \
+    template std::vector<double> simulate_terminals<P>(const P&, double, double, double,                     \
+                                                       const mc::SimulationPlan&);                            \
+    template std::vector<mc::PriceEstimate> price_european_batch<P>(const P&, double, const std::vector<double>&, \
+                                                                    double, double, double,                    \
+                                                                    const mc::SimulationPlan&);                \
+    template mc::PriceEstimate price_european_call<P>(const P&, double, double, double, double, double,       \
+                                                      const mc::SimulationPlan&);                              \
+    template mc::PriceEstimate price_cliquet<P>(const P&, double, double, double, const mc::CliquetSpec&,      \
+                                                const mc::SimulationPlan&);
+SABR_B200_MC(StaticSabrParams)
+SABR_B200_MC(CaseIParams)
+SABR_B200_MC(CaseIIParams)
+#undef SABR_B200_MC
 
 CalibrationReport calibrate_static_T1(const VolSurface& surface, std::size_t slice, const BoundsOverrides& bounds,
                                       const AnnealingSchedule& schedule, const FixedParams& fixed) {

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "sabr/calibration.hpp"
+#include "sabr/mc.hpp"
 
 namespace sabr::b200 {
 
@@ -26,5 +27,29 @@ CalibrationReport calibrate_case2_T2(const VolSurface& surface, const BoundsOver
                                      const FixedParams& fixed = {},
                                      const std::optional<mc::SimulationPlan>& report_plan = std::nullopt,
                                      const std::vector<double>* start_override = nullptr);
+
+// The Monte Carlo operator (mc.hpp:66-84).  mc::ModelDynamics keeps its
+// parameters private, so the device versions take the parameter structs the
+// dynamics are built from (ModelDynamics::from_static / from_case1 /
+// from_case2): a maintainer dispatches where the parameters are in hand
+// (case2_mc_cost, calibration.cpp:399-416; the CLI's price command), or adds
+// an accessor to ModelDynamics.  Same streams (xoshiro, block_size paths per
+// substream), same results to rounding.
+template <class Params>
+std::vector<double> simulate_terminals(const Params& p, double forward0, double alpha0, double maturity,
+                                       const mc::SimulationPlan& plan);
+
+template <class Params>
+std::vector<mc::PriceEstimate> price_european_batch(const Params& p, double spot, const std::vector<double>& strikes,
+                                                    double rate, double dividend, double maturity,
+                                                    const mc::SimulationPlan& plan);
+
+template <class Params>
+mc::PriceEstimate price_european_call(const Params& p, double spot, double strike, double rate, double dividend,
+                                      double maturity, const mc::SimulationPlan& plan);
+
+template <class Params>
+mc::PriceEstimate price_cliquet(const Params& p, double spot, double rate, double dividend,
+                                const mc::CliquetSpec& spec, const mc::SimulationPlan& plan);
 
 }  // namespace sabr::b200

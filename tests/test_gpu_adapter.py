@@ -5,7 +5,9 @@ binary calls sabr::calibrate_* (the reference, CPU) and sabr::b200::calibrate_*
 seeds and prints both CalibrationReports; they must agree the way the engine
 agrees with the reference everywhere else: the same trajectory (evals), the
 same parameters and cost to rounding, and the reference's exception types for
-its error cases (proj/tests/test_calibration.cpp:212-225)."""
+its error cases (proj/tests/test_calibration.cpp:212-225).  The same for the
+Monte Carlo operator (mc.hpp:66-84): prices, standard errors and terminals
+on the reference's streams."""
 import json
 import os
 import subprocess
@@ -47,7 +49,25 @@ def test_adapter_matches_reference(cases, name, cost_tol, param_tol):
         assert abs(g - r) <= 1e-8 * max(1.0, abs(r))
 
 
+@pytest.mark.parametrize("name", ["mc_static", "mc_case1", "mc_case2", "mc_cliquet"])
+def test_adapter_mc_matches_reference(cases, name):
+    """mc::price_european_batch / price_cliquet through the adapter: the
+    reference's streams, prices and standard errors to 1e-11 relative."""
+    c = cases[name]
+    assert len(c["b200"]) == len(c["ref"])
+    for (rv, rs), (gv, gs) in zip(c["ref"], c["b200"]):
+        for r, g in ((rv, gv), (rs, gs)):
+            r, g = float.fromhex(r), float.fromhex(g)
+            assert abs(g - r) <= 1e-11 * max(abs(r), 1e-12), (name, r, g)
+
+
+def test_adapter_mc_terminals(cases):
+    c = cases["mc_terminals"]
+    assert c["n"] == 10000
+    assert c["max_rel"] <= 1e-12
+
+
 def test_adapter_error_types(cases):
     c = cases["errors"]
     assert c["b200"] == c["ref"]
-    assert c["ref"] == ["out_of_range", "domain_error", "domain_error"]
+    assert c["ref"] == ["out_of_range", "domain_error", "domain_error", "domain_error"]
