@@ -89,6 +89,21 @@ int main(int argc, char** argv) {
     plan.seed = 1;
     emit("case2_T2", calibrate_case2_T2(one, {}, s4, plan, fixed), b200::calibrate_case2_T2(one, {}, s4, plan, fixed));
 
+    AnnealingSchedule s5 = s1;  // Case II formula objective (calibration.hpp:108-111), short schedule
+    s5.chain_length = 20;
+    s5.cooling = 0.7;
+    s5.t_min = 1e-3;
+    s5.seed = 4;
+    emit("case2_formula", calibrate_case2_formula(fx, {}, s5, {{"beta", 1.0}}),
+         b200::calibrate_case2_formula(fx, {}, s5, {{"beta", 1.0}}));
+    const CaseIParams e1{0.13, 1.0, -0.25, 0.9, 0.7, 1.1};
+    emit("evaluate_case1", evaluate_case1(fx, e1), b200::evaluate_case1(fx, e1));
+    const CaseIIParams e2{0.13, 1.0, -0.25, 0.05, 0.02, 0.9, -0.1, 0.05, 0.7, 1.1, fx.slices.back().maturity};
+    mc::SimulationPlan ep;
+    ep.num_paths = 1u << 14;
+    ep.seed = 5;
+    emit("evaluate_case2_prices", evaluate_case2_prices(fx, e2, ep), b200::evaluate_case2_prices(fx, e2, ep));
+
     // the Monte Carlo operator (mc.hpp:66-84): same streams, prices to rounding
     mc::SimulationPlan mp;
     mp.num_paths = 1u << 16;

@@ -226,4 +226,27 @@ CalibrationReport calibrate_case2_T2(const VolSurface& surface, const BoundsOver
     });
 }
 
+CalibrationReport calibrate_case2_formula(const VolSurface& surface, const BoundsOverrides& bounds,
+                                          const AnnealingSchedule& schedule, const FixedParams& fixed) {
+    const sabr_schedule sch = to_abi(schedule);
+    return run(surface, bounds, fixed, [&](sabr_ctx* c, const sabr_surface* s, const sabr_bounds* b,
+                                           const sabr_fixed* f, sabr_report* r) {
+        return sabr_calibrate_case2_formula(c, s, b, &sch, f, r);
+    });
+}
+
+CalibrationReport evaluate_case1(const VolSurface& surface, const CaseIParams& p) {
+    const ModelArgs m = model_args(p);
+    return run(surface, {}, {}, [&](sabr_ctx* c, const sabr_surface* s, const sabr_bounds*, const sabr_fixed*,
+                                    sabr_report* r) { return sabr_evaluate_case1(c, s, m.v.data(), r); });
+}
+
+CalibrationReport evaluate_case2_prices(const VolSurface& surface, const CaseIIParams& p,
+                                        const mc::SimulationPlan& plan) {
+    const ModelArgs m = model_args(p);
+    const sabr_plan pl = to_abi(plan);
+    return run(surface, {}, {}, [&](sabr_ctx* c, const sabr_surface* s, const sabr_bounds*, const sabr_fixed*,
+                                    sabr_report* r) { return sabr_evaluate_case2_prices(c, s, m.v.data(), &pl, r); });
+}
+
 }  // namespace sabr::b200

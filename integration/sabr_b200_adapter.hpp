@@ -28,6 +28,14 @@ CalibrationReport calibrate_case2_T2(const VolSurface& surface, const BoundsOver
                                      const std::optional<mc::SimulationPlan>& report_plan = std::nullopt,
                                      const std::vector<double>* start_override = nullptr);
 
+CalibrationReport calibrate_case2_formula(const VolSurface& surface, const BoundsOverrides& bounds,
+                                          const AnnealingSchedule& schedule, const FixedParams& fixed = {});
+
+CalibrationReport evaluate_case1(const VolSurface& surface, const CaseIParams& p);
+
+CalibrationReport evaluate_case2_prices(const VolSurface& surface, const CaseIIParams& p,
+                                        const mc::SimulationPlan& plan);
+
 // The Monte Carlo operator (mc.hpp:66-84).  mc::ModelDynamics keeps its
 // parameters private, so the device versions take the parameter structs the
 // dynamics are built from (ModelDynamics::from_static / from_case1 /

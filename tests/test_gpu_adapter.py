@@ -31,7 +31,10 @@ def cases():
 
 @pytest.mark.parametrize("name,cost_tol,param_tol", [("static_T1", 1e-12, 1e-9),
                                                      ("case1_T1", 1e-12, 1e-9),
-                                                     ("case2_T2", 1e-10, 1e-9)])
+                                                     ("case2_T2", 1e-10, 1e-9),
+                                                     ("case2_formula", 1e-10, 1e-7),
+                                                     ("evaluate_case1", 1e-12, 0.0),
+                                                     ("evaluate_case2_prices", 1e-10, 0.0)])
 def test_adapter_matches_reference(cases, name, cost_tol, param_tol):
     c = cases[name]
     ref, gpu = c["ref"], c["b200"]
