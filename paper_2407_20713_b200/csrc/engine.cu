@@ -894,6 +894,14 @@ int choose_ppt(const sabr_plan& plan) {
     return 1;
 }
 
+// every step of the grid has the same dt (no short last step)
+bool uniform_grid(const HostGrid& g) {
+    for (size_t i = 1; i < g.dt.size(); ++i)
+        if (std::memcmp(&g.dt[i], &g.dt[0], sizeof(double)) != 0 || std::memcmp(&g.sdt[i], &g.sdt[0], sizeof(double)) != 0)
+            return false;
+    return true;
+}
+
 std::vector<uint64_t> mc_layout(sabr_ctx* ctx, const sabr_plan& plan, int ppt,
                                 const std::vector<HostGrid>& grids, McJob& job) {
     std::vector<uint64_t> jump;
@@ -949,12 +957,16 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
         sl.lnf0 = std::log(sl.forward0);
         sl.discount = std::exp(-rate[s] * maturity[s]);
         const HostGrid& g = grids[s];
+        const size_t first = coef.size();
         for (size_t i = 0; i < g.dt.size(); ++i) {
             const double nu = model_nu_at(model, params, g.t_end[i]);
             const double rho = model_rho_at(model, params, g.t_end[i]);
             const double srho = std::sqrt(std::max(0.0, 1.0 - rho * rho));
             coef.push_back({nu * g.sdt[i], 0.5 * nu * nu * g.dt[i], rho * g.sdt[i], srho * g.sdt[i]});
         }
+        sl.const_coef = uniform_grid(g) && std::all_of(coef.begin() + first, coef.end(), [&](const StepCoef& c) {
+                            return std::memcmp(&c, &coef[first], sizeof(StepCoef)) == 0;
+                        });
     }
     const int nq = static_cast<int>(strikes.size());
     McParams P{};
@@ -971,6 +983,7 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     P.block_size = plan.block_size;
     P.seed = plan.seed;
     P.slices = upload(ctx, "mc_slices", job.slices);
+    P.host_slices = job.slices.data();
     const double beta = params[1];
     P.alpha0 = upload(ctx, "mc_alpha0", std::vector<double>{alpha0});
     P.beta = upload(ctx, "mc_beta", std::vector<double>{beta});

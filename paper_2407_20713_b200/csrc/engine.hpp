@@ -90,6 +90,8 @@ struct HostGrid {
     std::vector<double> dt, sdt, t_end;
 };
 HostGrid build_grid(double maturity, double dt);
+// every step of the grid has the same dt (no short last step)
+bool uniform_grid(const HostGrid& g);
 
 // Host-side CaseIIParams::validate with the reference message (input
 // validation before a device run; the SA hot loop uses the device predicate).

@@ -31,7 +31,10 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int CB>
+// CONST: every slice of the launch has time-invariant step rows (McSlice::
+// const_coef): the first row and dt serve every step, no per-step loads.  A
+// separate instantiation, so the general kernel's code is unchanged.
+template <int CB, bool CONST>
 __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_constant__ McParams P) {
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
@@ -153,15 +156,25 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
             double z1, z2;
             normals(0, z1, z2);
             const int n = sl.n_steps;
-            for (int i = 0; i + 1 < n; ++i) {
-                double n1, n2;
-                normals(i + 1, n1, n2);
-                const double hn = __ldg(hdt + i + 1);
-                crow += cstride;
-                advance_all(h, z1, z2, crow);
-                h = hn;
-                z1 = n1;
-                z2 = n2;
+            if constexpr (CONST) {
+                for (int i = 0; i + 1 < n; ++i) {
+                    double n1, n2;
+                    normals(i + 1, n1, n2);
+                    advance_all(h, z1, z2, nullptr);
+                    z1 = n1;
+                    z2 = n2;
+                }
+            } else {
+                for (int i = 0; i + 1 < n; ++i) {
+                    double n1, n2;
+                    normals(i + 1, n1, n2);
+                    const double hn = __ldg(hdt + i + 1);
+                    crow += cstride;
+                    advance_all(h, z1, z2, crow);
+                    h = hn;
+                    z1 = n1;
+                    z2 = n2;
+                }
             }
             advance_all(h, z1, z2, nullptr);
         }
@@ -538,7 +551,9 @@ template <int CB>
 cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     const int mq = p.max_q;
     const size_t smem = p.partials ? static_cast<size_t>(kWarps) * CB * mq * 2 * sizeof(double) : 0;
-    auto k = p.fp32 ? mc_tile_kernel_f32<CB> : mc_tile_kernel<CB>;
+    bool cst = p.n_slices > 0;
+    for (int i = 0; i < p.n_slices; ++i) cst = cst && p.host_slices != nullptr && p.host_slices[i].const_coef;
+    auto k = p.fp32 ? mc_tile_kernel_f32<CB> : (cst ? mc_tile_kernel<CB, true> : mc_tile_kernel<CB, false>);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));

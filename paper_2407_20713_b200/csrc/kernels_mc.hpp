@@ -17,6 +17,9 @@ struct McSlice {
     double forward0;   // S*exp((r-y)T), mc.cpp:258
     double lnf0;       // log(forward0)
     double discount;   // exp(-rT), mc.cpp:262
+    int32_t const_coef;  // every step row of this slice equals its first (time-invariant
+                         // dynamics on a uniform grid): the FP64 kernel loads it once
+    int32_t _pad;
 };
 
 // Per-step, per-candidate log-Euler coefficients (mc.cpp:97-102) for the
@@ -43,6 +46,7 @@ struct McParams {
     uint64_t block_size;
     uint64_t seed;
     const McSlice* slices;  // [n_slices]
+    const McSlice* host_slices;  // [n_slices] host copy (launch-time choices), or null
     const double* alpha0;   // [n_cand]
     const double* beta;     // [n_cand]
     const uint8_t* active;  // [n_cand] or null: inactive candidates (zero coefficients)

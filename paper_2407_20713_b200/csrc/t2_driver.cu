@@ -66,9 +66,15 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     McJob job;
     job.slices.resize(ns);
     const auto jump = mc_layout(ctx, plan, ppt, grids, job);
+    // time-invariant dynamics for every chain: q_rho, q_nu, a, b (CaseIIParams
+    // indices 3, 6, 8, 9) fixed at 0, so rho(t) = rho0 + d_rho, nu(t) = nu0 + d_nu
+    // (analytics.cpp:138-143) and a uniform grid gives identical step rows
+    bool invariant = true;
+    for (int i : {3, 6, 8, 9}) invariant = invariant && !ps.is_free[i] && start_full[i] == 0.0;
     std::vector<double> t_end, dt, sdt;
     for (size_t s = 0; s < ns; ++s) {
         McSlice& sl = job.slices[s];
+        sl.const_coef = invariant && uniform_grid(grids[s]);
         sl.q_begin = static_cast<int32_t>(surface.off[s]);
         sl.q_end = static_cast<int32_t>(surface.off[s + 1]);
         job.max_q = std::max(job.max_q, sl.q_end - sl.q_begin);
@@ -114,6 +120,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     P.block_size = plan.block_size;
     P.seed = plan.seed;
     P.slices = upload(ctx, "t2_slices", job.slices);
+    P.host_slices = job.slices.data();
     P.hdt = upload(ctx, "t2_hdt", job.hdt);
     P.strikes = upload(ctx, "t2_strikes", surface.K);
     P.jump = upload(ctx, "t2_jump", jump);
