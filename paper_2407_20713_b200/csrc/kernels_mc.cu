@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
 // reference draws them), the same log-Euler step carried in FP32 state with
 // one MUFU ex2 per candidate-step; normals from accurate FP32 library
 // functions; F_T = F0 exp(x) and the payoff sums in FP64.
-template <int CB>
+template <int CB, bool CONST>
 __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid_constant__ McParams P) {
     extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
 
@@ -325,6 +325,17 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
             float z1, z2;
             normals(0, z1, z2);
             const int n = sl.n_steps;
+            if constexpr (CONST) {  // time-invariant rows (McSlice::const_coef): loaded once
+#pragma unroll 2
+                for (int i = 0; i + 1 < n; ++i) {
+                    float n1, n2;
+                    normals(i + 1, n1, n2);
+                    advance_all(hn, qn, z1, z2);
+                    z1 = n1;
+                    z2 = n2;
+                }
+                advance_all(hn, qn, z1, z2);
+            } else {
             // unrolled by 2 so the q <- qn rotation is register renaming, not
             // 4*CB moves per step (392 -> 341 instructions per step at CB = 8)
 #pragma unroll 2
@@ -343,6 +354,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
                 z2 = n2;
             }
             advance_all(hn, qn, z1, z2);
+            }
         }
         double F[CB];
 #pragma unroll
@@ -553,7 +565,8 @@ cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     const size_t smem = p.partials ? static_cast<size_t>(kWarps) * CB * mq * 2 * sizeof(double) : 0;
     bool cst = p.n_slices > 0;
     for (int i = 0; i < p.n_slices; ++i) cst = cst && p.host_slices != nullptr && p.host_slices[i].const_coef;
-    auto k = p.fp32 ? mc_tile_kernel_f32<CB> : (cst ? mc_tile_kernel<CB, true> : mc_tile_kernel<CB, false>);
+    auto k = p.fp32 ? (cst ? mc_tile_kernel_f32<CB, true> : mc_tile_kernel_f32<CB, false>)
+                    : (cst ? mc_tile_kernel<CB, true> : mc_tile_kernel<CB, false>);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
