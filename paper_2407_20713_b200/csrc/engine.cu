@@ -209,6 +209,7 @@ struct T1Out {
 // free_mask are searched.
 using StartFn = std::function<cudaError_t(const SaLevelArgs&)>;
 using LevelFn = std::function<cudaError_t(const SaLevelArgs&, int64_t, double)>;
+using RunAllFn = std::function<cudaError_t(const SaLevelArgs&, const double*, int64_t)>;
 
 // The device-resident level loop shared by every T_I-style objective:
 // `start` seeds incumbent/best values on the device, `level` launches one
@@ -218,7 +219,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
                      const std::vector<double>& hi, const std::vector<double>& start_full,
                      const sabr_schedule& sch, bool start_ok, int64_t records,
                      const StartFn& start, const LevelFn& level_fn, int builtin, int pred,
-                     bool use_peer = false) {
+                     bool use_peer = false, const RunAllFn& run_all = nullptr) {
     validate_schedule(sch);
     // SearchSpace::validate, annealer.cpp:48-58
     if (free_mask == 0) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
@@ -299,7 +300,17 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     timer.start();
     int64_t launched = 0;
     auto* done_flag = static_cast<int64_t*>(ctx->pinned);
-    for (int64_t level = 0; level < L; ++level) {
+    int64_t first_level = 0;
+    if (run_all && L > 0 && a.n_local > 0 && ctx->nranks == 1 && run_all(a, nullptr, L) == cudaSuccess) {
+        // one launch for every level (a one-CTA run)
+        const double* temps_dev = upload(ctx, "sa_temps", temps);
+        timer.before();
+        check_cuda(run_all(a, temps_dev, L), "sa_run_small");
+        timer.after();
+        ++launched;
+        first_level = L;
+    }
+    for (int64_t level = first_level; level < L; ++level) {
         NvtxRange nvtx_level("sabr.level");
         if (a.n_local > 0) {
             timer.before();
@@ -357,7 +368,10 @@ T1Out run_sa_t1(sabr_ctx* ctx, int kind, const SurfaceView& sv, int dim_full, ui
         [&](const SaLevelArgs& a, int64_t level, double temp) {
             return launch_sa_level(kind, sv, a, level, temp, s);
         },
-        builtin, pred, /*use_peer=*/true);
+        builtin, pred, /*use_peer=*/true,
+        [&](const SaLevelArgs& a, const double* temps, int64_t n_levels) {
+            return launch_sa_run_small(kind, sv, a, temps, n_levels, s);
+        });
 }
 
 // GaussLegendreRule(n), proj/src/quadrature.cpp:13-33 (same Newton iteration,

@@ -104,6 +104,11 @@ cudaError_t launch_sa_level(int kind, const SurfaceView& sv, const SaLevelArgs& 
 cudaError_t launch_sa_merge(const SaLevelArgs& a, const sabr_level_record* recs, int64_t level,
                             cudaStream_t s);
 // Evaluate the objective at state->incumbent and seed incumbent/best values.
+// All levels of a one-CTA, one-rank run in one launch (sa_run_small_kernel);
+// cudaErrorNotSupported when the run does not qualify (then launch per level).
+// temps == nullptr: only report whether it qualifies.
+cudaError_t launch_sa_run_small(int kind, const SurfaceView& sv, const SaLevelArgs& a, const double* temps,
+                                int64_t n_levels, cudaStream_t s);
 cudaError_t launch_sa_start(int kind, const SurfaceView& sv, const SaLevelArgs& a,
                             cudaStream_t s);
 // cost[i] of full parameter vectors params[i*dim_full ..].

@@ -915,53 +915,18 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
 constexpr int kPairMinCtas = 11;
 constexpr int kMaxPwSlices = 64;
 
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
-__global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
-    sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
-                          const int64_t level, const double temp, const double inv_temp) {
-    constexpr int NT = kLevelThreads / C;
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ RedShared<NT> rs;
-    __shared__ sabr_level_record rec;
-    __shared__ double2 tab_s[kExpTableSize];
-    __shared__ double bp_s[C][DIMF][NT];
-
-    sabr_sa_state* st = a.state;
-    // Programmatic dependent launch: the next level's grid may start as soon
-    // as SMs free up; everything before pdl_wait() (table and grid staging,
-    // the chains' stream seeding) does not depend on the previous level and
-    // overlaps its tail (the last CTA's merge).  Nothing written by the
-    // previous level is read before pdl_wait().
-    pdl_trigger();
-    stage_exp(sv, tab_s);
-    ObjGrid<GK> g = stage_obj<GK>(sv, smem);
-    __syncthreads();
-    g.tab = tab_s;
-
-    bool active[C];
-    int64_t chain[C];
-    Xoshiro rng[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-        const int64_t local = static_cast<int64_t>(blockIdx.x) * (NT * C) + c * NT + threadIdx.x;
-        active[c] = local < a.n_local;
-        chain[c] = a.chain_begin + local;
-        // substream keyed by (seed, level, chain): annealer.cpp:112-115
-        rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
-    }
-    pdl_wait();
-    if (st->done) return;  // early-stopped run (max_evals): uniform exit
-    // Case I with beta not searched: f_i^(1-beta) is one value per slice
-    __shared__ double pw_s[kMaxPwSlices];
-    const double* pw_fixed = nullptr;
-    if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
-        if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {
-            const double omb = 1.0 - st->incumbent[1];
-            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
-            __syncthreads();
-            pw_fixed = pw_s;
-        }
-    }
+// The chains of one CTA for one level (annealer.cpp:107-139) and the CTA's
+// level-end arg-min (annealer.cpp:141-159): on return (all threads) rs holds
+// the CTA's (endpoint, best) winners and eval count, rec their points.
+// Shared by the per-level kernel and the single-CTA persistent kernel.
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT>
+__device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const ObjGrid<GK>& g,
+                                                 const double2* tab_s, const double* pw_fixed,
+                                                 const sabr_sa_state* st, const double temp,
+                                                 const double inv_temp, const bool (&active)[C],
+                                                 const int64_t (&chain)[C], Xoshiro (&rng)[C],
+                                                 double (&bp_s)[C][DIMF][NT], RedShared<NT>& rs,
+                                                 sabr_level_record& rec) {
     double x[C][DIMF], y[C][DIMF], fx[C], bv[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -1060,8 +1025,129 @@ __global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
         }
     }
     __syncthreads();
+}
+
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
+__global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
+    sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
+                          const int64_t level, const double temp, const double inv_temp) {
+    constexpr int NT = kLevelThreads / C;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RedShared<NT> rs;
+    __shared__ sabr_level_record rec;
+    __shared__ double2 tab_s[kExpTableSize];
+    __shared__ double bp_s[C][DIMF][NT];
+
+    sabr_sa_state* st = a.state;
+    // Programmatic dependent launch: the next level's grid may start as soon
+    // as SMs free up; everything before pdl_wait() (table and grid staging,
+    // the chains' stream seeding) does not depend on the previous level and
+    // overlaps its tail (the last CTA's merge).  Nothing written by the
+    // previous level is read before pdl_wait().
+    pdl_trigger();
+    stage_exp(sv, tab_s);
+    ObjGrid<GK> g = stage_obj<GK>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
+
+    bool active[C];
+    int64_t chain[C];
+    Xoshiro rng[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int64_t local = static_cast<int64_t>(blockIdx.x) * (NT * C) + c * NT + threadIdx.x;
+        active[c] = local < a.n_local;
+        chain[c] = a.chain_begin + local;
+        // substream keyed by (seed, level, chain): annealer.cpp:112-115
+        rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
+    }
+    pdl_wait();
+    if (st->done) return;  // early-stopped run (max_evals): uniform exit
+    // Case I with beta not searched: f_i^(1-beta) is one value per slice
+    __shared__ double pw_s[kMaxPwSlices];
+    const double* pw_fixed = nullptr;
+    if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
+        if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {
+            const double omb = 1.0 - st->incumbent[1];
+            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            __syncthreads();
+            pw_fixed = pw_s;
+        }
+    }
+    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, pw_fixed, st, temp, inv_temp, active, chain,
+                                                     rng, bp_s, rs, rec);
     if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
     reduce_block_records<NT, DIMF>(rs, a, level);
+}
+
+// Every level of a run whose chains fit one CTA (C1: 32 chains), on one rank,
+// in one launch: the per-level launch, the grid-level record scan and the
+// level-to-level dependency (8.3 us per level at C1) collapse into a
+// __syncthreads.  Per level: the same chains and arg-min as
+// sa_level_multi_kernel, then thread 0 applies merge_level to the CTA record
+// (what reduce_block_records does for a one-CTA grid).  temps[level] is the
+// host's schedule (annealer.cpp:99, repeated multiplication), 1/T as the host
+// computes it.  Identical trajectories to the per-level kernels.
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
+__global__ void __launch_bounds__(kLevelThreads / C, 1)
+    sa_run_small_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
+                        const double* __restrict__ temps, const int64_t n_levels) {
+    constexpr int NT = kLevelThreads / C;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ RedShared<NT> rs;
+    __shared__ sabr_level_record rec;
+    __shared__ double2 tab_s[kExpTableSize];
+    __shared__ double bp_s[C][DIMF][NT];
+    __shared__ double pw_s[kMaxPwSlices];
+    sabr_sa_state* st = a.state;
+    stage_exp(sv, tab_s);
+    ObjGrid<GK> g = stage_obj<GK>(sv, smem);
+    __syncthreads();
+    g.tab = tab_s;
+    bool active[C];
+    int64_t chain[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int64_t local = static_cast<int64_t>(c) * NT + threadIdx.x;
+        active[c] = local < a.n_local;
+        chain[c] = a.chain_begin + local;
+    }
+    const double* pw_fixed = nullptr;
+    if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
+        if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {  // beta not searched: constant
+            const double omb = 1.0 - st->incumbent[1];
+            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            __syncthreads();
+            pw_fixed = pw_s;
+        }
+    }
+    for (int64_t level = 0; level < n_levels; ++level) {
+        if (st->done) break;  // block-uniform (merge_level's writes are behind the __syncthreads)
+        const double temp = temps[level];
+        const double inv_temp = 1.0 / temp;
+        Xoshiro rng[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
+        run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, pw_fixed, st, temp, inv_temp, active, chain,
+                                                         rng, bp_s, rs, rec);
+        if (threadIdx.x == 0) {
+            sabr_level_record out;
+            const bool e_ok = rs.e_win.i != LLONG_MAX, b_ok = rs.b_win.i != LLONG_MAX;
+            out.end_value = rs.e_win.v;
+            out.end_chain = e_ok ? rs.e_win.i : -1;
+            out.best_value = rs.b_win.v;
+            out.best_chain = b_ok ? rs.b_win.i : -1;
+            out.evals = rs.n_tot;
+            out._pad = 0;
+            for (int i = 0; i < SABR_MAX_DIM; ++i) {
+                out.end_point[i] = e_ok && i < DIMF ? rec.end_point[i] : 0.0;
+                out.best_point[i] = b_ok && i < DIMF ? rec.best_point[i] : 0.0;
+            }
+            merge_level(st, &out, 1, a.n_chains, a.max_evals, a.levels_total, DIMF, a.trace_f + level);
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void sa_merge_kernel(const SaLevelArgs a, const sabr_level_record* recs,
@@ -1452,6 +1538,36 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
         sv, [](auto smem) { return sa_level_kernel<KIND, DIMF, false, decltype(smem)::value>; }, run);
 }
 
+// SABR_SA_PERSIST=0 disables the one-launch path for one-CTA runs (A/B checks).
+bool persist_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SABR_SA_PERSIST");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
+template <int KIND, int DIMF>
+cudaError_t run_small_t(const SurfaceView& sv, const SaLevelArgs& a, const double* temps, int64_t n_levels,
+                        cudaStream_t s) {
+    constexpr int C = 1;
+    if constexpr (KIND == OBJ_BUILTIN) {
+        return cudaErrorNotSupported;
+    } else {
+        size_t smem = 0;
+        if (!persist_enabled() || a.nranks != 1 || a.n_local > kLevelThreads / C || grid_kind(sv, &smem) != kGridQR)
+            return cudaErrorNotSupported;
+        if (temps == nullptr) return cudaSuccess;  // eligibility query
+        const bool all_free = a.fast != 0 && a.free_mask == (1u << DIMF) - 1u && sv.max_abs_lnf <= 700.0;
+        auto k = all_free ? sa_run_small_kernel<KIND, DIMF, true, kGridQR, C>
+                          : sa_run_small_kernel<KIND, DIMF, false, kGridQR, C>;
+        cudaError_t e = set_smem(k, smem);
+        if (e != cudaSuccess) return e;
+        k<<<1, kLevelThreads / C, smem, s>>>(sv, a, temps, n_levels);
+        return cudaGetLastError();
+    }
+}
+
 template <int KIND, int DIMF>
 cudaError_t start_t(const SurfaceView& sv, const SaLevelArgs& a, cudaStream_t s) {
     return dispatch_grid<KIND>(
@@ -1516,6 +1632,13 @@ int t2_block_threads() { return kThreads; }
 cudaError_t launch_sa_level(int kind, const SurfaceView& sv, const SaLevelArgs& a, int64_t level,
                             double temp, cudaStream_t s) {
 #define CALL(K, D) level_t<K, D>(sv, a, level, temp, s)
+    SABR_DISPATCH(kind, a.dim_full, CALL);
+#undef CALL
+}
+
+cudaError_t launch_sa_run_small(int kind, const SurfaceView& sv, const SaLevelArgs& a, const double* temps,
+                                int64_t n_levels, cudaStream_t s) {
+#define CALL(K, D) run_small_t<K, D>(sv, a, temps, n_levels, s)
     SABR_DISPATCH(kind, a.dim_full, CALL);
 #undef CALL
 }

@@ -45,14 +45,26 @@ out["case1"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r
 r = eng.calibrate_dynamic_case1_T1(eq, None, s3, {"beta": 0.7}, trace=True)
 out["case1_beta_fixed"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
                            [f.hex() for _, f in r.temperature_trace]]
+# one-CTA runs (<= 64 chains): every level in one launch unless SABR_SA_PERSIST=0
+s4 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=2)
+r = eng.calibrate_static_T1(eq, 1, None, s4, None, trace=True)
+out["small_static"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                       [f.hex() for _, f in r.temperature_trace]]
+s5 = pkg.AnnealingSchedule(t0=2.0, cooling=0.9, chain_length=50, workers=21, groups=3, t_min=1e-5, seed=7,
+                           max_evals=150000)
+r = eng.calibrate_dynamic_case1_T1(fx, None, s5, {"beta": 1.0}, trace=True)
+out["small_case1_cap"] = [r.final_cost.hex(), {k: v.hex() for k, v in r.params.items()}, r.evals,
+                          [f.hex() for _, f in r.temperature_trace]]
 print(json.dumps(out))
 """
 
 
-def run_variant(cpt, fast=None, cost=None):
+def run_variant(cpt, fast=None, cost=None, persist=None):
     env = dict(os.environ)
-    for k in ("SABR_SA_CPT", "SABR_SA_FAST", "SABR_SA_COST"):
+    for k in ("SABR_SA_CPT", "SABR_SA_FAST", "SABR_SA_COST", "SABR_SA_PERSIST"):
         env.pop(k, None)
+    if persist is not None:
+        env["SABR_SA_PERSIST"] = str(persist)
     if cpt is not None:
         env["SABR_SA_CPT"] = str(cpt)
     if fast is not None:
@@ -101,3 +113,12 @@ def test_fast_propose_matches_general_propose():
     general = run_variant(None, fast=0)
     for k in fast:
         assert fast[k] == general[k], k
+
+
+def test_one_launch_run_matches_per_level_launches():
+    """sa_run_small_kernel (all levels of a one-CTA run in one launch, with an
+    eval cap reached inside a level) against the per-level kernels."""
+    persistent = run_variant(None)
+    per_level = run_variant(None, persist=0)
+    for k in persistent:
+        assert persistent[k] == per_level[k], k
