@@ -104,7 +104,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     int cb = chunk >= 8 ? 8 : (chunk >= 4 ? 4 : (chunk >= 2 ? 2 : 1));
     if (const char* e = std::getenv("SABR_MC_CB")) {  // tuning override (1, 2, 4, 8, 16)
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) cb = std::min(v, cb);
+        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) cb = v;
     }
     const int32_t stride = (chunk + cb - 1) / cb * cb;  // coefficient row width
 
