@@ -347,7 +347,7 @@ def run_ours(args):
         "gpu_launches": int(launches_tot),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "sa_level_multi_kernel<OBJ_STATIC,4,ALLFREE,QR> (2 chains per thread, factored slice cost)",
+                     "kernel": "sa_level_multi_kernel<OBJ_STATIC,4,ALLFREE,QR,3> (3 chains per thread, factored slice cost)",
                      "avg_launch_ms": avg_launch_s * 1e3, "launches": klaunch_tot,
                      "flops_per_eval": per_eval["flops"], "flops_source": per_eval["source"],
                      "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "

@@ -913,6 +913,13 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
 // (SABR_SA_CPT=1, factored grid only): 64-thread CTAs.  1e5 chains: 1563
 // CTAs, 11 per SM, in one wave either way.
 constexpr int kPairMinCtas = 11;
+// threads per CTA and CTAs per SM (launch bound) of the C-chain level kernel:
+// C = 1, 2 cover kLevelThreads chains per CTA; C = 3 (SABR_SA_CPT=3, A/B)
+// uses one warp of 96 chains and 8 CTAs per SM (<= 255 registers)
+template <int C>
+constexpr int level_nt() { return C == 3 ? 32 : kLevelThreads / C; }
+template <int C>
+constexpr int level_min_ctas() { return C == 3 ? 8 : kPairMinCtas; }
 constexpr int kMaxPwSlices = 64;
 
 // The chains of one CTA for one level (annealer.cpp:107-139) and the CTA's
@@ -1028,10 +1035,10 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
 }
 
 template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
-__global__ void __launch_bounds__(kLevelThreads / C, kPairMinCtas)
+__global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
-    constexpr int NT = kLevelThreads / C;
+    constexpr int NT = level_nt<C>();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
     __shared__ sabr_level_record rec;
@@ -1467,15 +1474,15 @@ cudaError_t dispatch_grid(const SurfaceView& sv, Pick&& pick, Body&& body) {
     }
 }
 
-// Chains per thread of the model-objective level kernel: SABR_SA_CPT=1 or 2
-// (default 2); SABR_SA_CPT=0 selects the general one-chain kernel
-// sa_level_kernel (A/B checks).
+// Chains per thread of the model-objective level kernel: SABR_SA_CPT=1, 2 or
+// 3; SABR_SA_CPT=0 selects the general one-chain kernel sa_level_kernel (A/B
+// checks).  -1 when unset: the default per objective (level_t).
 int chains_per_thread() {
     static const int c = [] {
         const char* e = std::getenv("SABR_SA_CPT");
-        if (!e) return 2;
+        if (!e) return -1;
         const int v = std::atoi(e);
-        return v == 0 || v == 1 ? v : 2;
+        return v == 0 || v == 1 || v == 3 ? v : 2;
     }();
     return c;
 }
@@ -1505,7 +1512,11 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
     if constexpr (KIND != OBJ_BUILTIN) {
         size_t smem = 0;
         const int gk = grid_kind(sv, &smem);
-        const int cpt = chains_per_thread();
+        // default: three chains per thread for the static objective (one warp
+        // of 96 chains per CTA: C2 7.28e10 -> 7.47e10 evals/s), two for Case I
+        // (three: 1.53e10 -> 1.34e10) and for the per-quote grid
+        const int cpt = chains_per_thread() >= 0 ? chains_per_thread()
+                                                 : (KIND == OBJ_STATIC && gk == kGridQR ? 3 : 2);
         if ((gk == kGridQR && cpt > 0) || (gk == kGridQuads && cpt == 2)) {
             using K = decltype(&sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 2>);
             const K kq2[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2>,
@@ -1514,8 +1525,12 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
                               sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 1>};
             const K kp2[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQuads, 2>,
                               sa_level_multi_kernel<KIND, DIMF, true, kGridQuads, 2>};
-            const K k = (gk == kGridQR ? (cpt == 1 ? kq1 : kq2) : kp2)[all_free ? 1 : 0];
-            const unsigned threads = static_cast<unsigned>(kLevelThreads / cpt);
+            const K kq3[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 3>,
+                              sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 3>};
+            const K k = (gk == kGridQR ? (cpt == 1 ? kq1 : cpt == 3 ? kq3 : kq2) : kp2)[all_free ? 1 : 0];
+            const int ntc = gk == kGridQR && cpt == 3 ? 3 : (gk == kGridQR && cpt == 1 ? 1 : 2);
+            const unsigned threads = static_cast<unsigned>(ntc == 3 ? level_nt<3>() : ntc == 1 ? level_nt<1>() : level_nt<2>());
+            const unsigned grid = static_cast<unsigned>((a.n_local + threads * ntc - 1) / (threads * ntc));
             cudaError_t e = set_smem(k, smem);
             if (e != cudaSuccess) return e;
             cudaLaunchConfig_t cfg{};

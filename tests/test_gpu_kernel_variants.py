@@ -1,6 +1,7 @@
 """The T_I level kernel variants must produce bit-identical annealer
-trajectories: two chains per thread (default), one chain per thread in the
-same kernel (SABR_SA_CPT=1) and the general one-chain kernel (SABR_SA_CPT=0);
+trajectories: three chains per thread (the static default), two (the Case I
+default), one chain per thread in the same kernel (SABR_SA_CPT=1) and the
+general one-chain kernel (SABR_SA_CPT=0);
 the FAST propose/exp path (one reflection, unsaturated exp; kernels_sa.cu
 propose_coord_fast) vs the general one (SABR_SA_FAST=0).  The factored slice
 cost (slice_qr.hpp, default) and the per-quote sum (SABR_SA_COST=quotes)
@@ -80,7 +81,7 @@ def run_variant(cpt, fast=None, cost=None, persist=None):
 @pytest.mark.parametrize("cost", [None, "quotes"])
 def test_multi_chain_kernel_matches_single_chain_kernels(cost):
     multi = run_variant(None, cost=cost)
-    for cpt in ((1, 0) if cost is None else (0,)):
+    for cpt in ((1, 0, 2, 3) if cost is None else (0,)):
         single = run_variant(cpt, cost=cost)
         assert multi.keys() == single.keys()
         for k in multi:
