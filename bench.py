@@ -475,14 +475,18 @@ def secondary(eng, torch, dev, stream):
     eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
     s1 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=1)
     eng.calibrate_static_T1(eq, 0, None, s1, None)
-    e0.record(stream)
-    rep = eng.calibrate_static_T1(eq, 0, None, s1, None)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    secs = e0.elapsed_time(e1) / 1e3
+    runs = []
+    for _ in range(5):  # a ~10 ms call: the median of five
+        e0.record(stream)
+        rep = eng.calibrate_static_T1(eq, 0, None, s1, None)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        runs.append(e0.elapsed_time(e1) / 1e3)
+    secs = float(np.median(runs))
     out["c1_static_calibration"] = {"metric": "calibrate_static_T1 wall time, C1 (EURO STOXX 50 slice 0, 32 chains)",
                                     "unit": "s", "value": secs, "cost_evals": rep.evals - 1,
-                                    "cost_evals_per_s": (rep.evals - 1) / secs, "final_cost": rep.final_cost}
+                                    "cost_evals_per_s": (rep.evals - 1) / secs, "final_cost": rep.final_cost,
+                                    "runs_s": runs, "statistic": "median of 5"}
     # C3: Case I joint calibration, EUR/USD, beta = 1 (acceptance.cpp:317-339 schedule, 1e5 chains)
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
     s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8, t_min=1e-7,
