@@ -1,5 +1,6 @@
 // slice_qr_check.cpp — host check of the factored slice cost (slice_qr.hpp):
-// for random market grids of n = 1 .. 600 quotes and random coefficient
+// for random market grids of n = 1 .. 600 quotes (and grids of repeated
+// strikes, whose factor is rank-deficient) and random coefficient
 // vectors (C0, A1, A2), ||R (C0, A1, A2, -1)||^2 evaluated as the kernels do
 // (nine FMAs) against the per-quote sum in x86 long double, next to the
 // per-quote sum in double (the reference's arithmetic).  Mixed error
@@ -25,6 +26,8 @@ int main() {
                 l[j] = -0.4 + 0.8 * U(gen);
                 m[j] = 0.05 + 0.6 * U(gen);
             }
+            if (rep == 19)  // repeated strikes: collinear columns, a rank-deficient factor
+                for (int j = 1; j < n; ++j) l[j] = l[j % 2];
             double R[sabr_gpu::kQrStride];
             sabr_gpu::slice_qr_factor(l.data(), m.data(), n, R);
             for (int t = 0; t < 2000; ++t) {
