@@ -237,6 +237,7 @@ def run_ours(args):
             eng.disable_peer_exchange()
     else:
         transport = "none (1 rank)"
+    print(f"bench rank {rank}/{world}: device cuda:{local}, transport: {transport}", file=sys.stderr, flush=True)
     eng.set_profiling(True)
 
     fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
@@ -573,6 +574,26 @@ def run_reference(args):
     }), flush=True)
 
 
+def launch_plan(gpus, env, argv):
+    """How `bench.py --gpus N` runs: ("run", None) in this process, ("exec",
+    cmd) to re-launch itself under torch.distributed.run with N ranks (when
+    started without a launcher), or ("error", msg) when a launcher's
+    WORLD_SIZE disagrees with --gpus (--gpus is authoritative)."""
+    if gpus < 1:
+        return "error", f"--gpus must be >= 1 (got {gpus})"
+    world = env.get("WORLD_SIZE")
+    if world is None:
+        if gpus == 1:
+            return "run", None
+        port = env.get("MASTER_PORT", "29531")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+        return "exec", cmd
+    if int(world) != gpus:
+        return "error", f"WORLD_SIZE={world} but --gpus {gpus}: launch one rank per GPU"
+    return "run", None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -582,6 +603,12 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    what, detail = launch_plan(args.gpus, os.environ, sys.argv[1:])
+    if what == "error":
+        print(f"bench.py: {detail}", file=sys.stderr)
+        sys.exit(2)
+    if what == "exec":
+        os.execv(detail[0], detail)
     if args.impl == "reference":
         run_reference(args)
     else:

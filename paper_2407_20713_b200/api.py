@@ -371,10 +371,17 @@ class _ReportBuf:
                                  r.wall_seconds, r.evals, r.seed, trace)
 
 
-def n_levels(schedule: AnnealingSchedule) -> int:
-    """Number of temperature levels, annealer.cpp:99-100 (repeated product)."""
+def n_levels(schedule: AnnealingSchedule, all_evals: bool = True) -> int:
+    """Number of temperature levels, annealer.cpp:99-100 (repeated product).
+    all_evals: every step is an evaluation (no feasibility predicate), so the
+    run stops after at most ceil((max_evals - 1) / n_chains) + 1 levels
+    (host_common.hpp: level_cap_all_evals)."""
+    chains = schedule.workers * schedule.groups
+    cap = None
+    if all_evals and chains > 0 and schedule.max_evals >= 1:
+        cap = (schedule.max_evals - 1 + chains - 1) // chains + 1
     n, t = 0, schedule.t0
-    while t >= schedule.t_min:
+    while t >= schedule.t_min and (cap is None or n < cap):
         n += 1
         t *= schedule.cooling
     return n
@@ -500,7 +507,7 @@ class Engine:
         s, keep = surface.to_abi()
         b, kb = _bounds_abi(bounds)
         f, kf = _fixed_abi(fixed)
-        rb = _ReportBuf(surface.total_quotes(), n_levels(schedule) if trace else 0)
+        rb = _ReportBuf(surface.total_quotes(), n_levels(schedule, all_evals=False) if trace else 0)
         sch, pl = schedule.to_abi(), plan.to_abi()
         rp = C.byref(report_plan.to_abi()) if report_plan is not None else None
         if start_override is not None:
@@ -520,7 +527,7 @@ class Engine:
         s, keep = surface.to_abi()
         b, kb = _bounds_abi(bounds)
         f, kf = _fixed_abi(fixed)
-        rb = _ReportBuf(surface.total_quotes(), n_levels(schedule) if trace else 0)
+        rb = _ReportBuf(surface.total_quotes(), n_levels(schedule, all_evals=False) if trace else 0)
         sch = schedule.to_abi()
         self._check(self.lib.sabr_calibrate_case2_formula(self._ctx, C.byref(s), C.byref(b),
                                                           C.byref(sch), C.byref(f),
@@ -649,7 +656,7 @@ class Engine:
         st = np.asarray(start, dtype=np.float64)
         dim = len(lo)
         best = np.zeros(max(1, dim))
-        cap = n_levels(schedule) if schedule.t0 > 0 and 0 < schedule.cooling < 1 and schedule.t_min > 0 else 1
+        cap = n_levels(schedule, predicate == A.PRED_NONE) if schedule.t0 > 0 and 0 < schedule.cooling < 1 and schedule.t_min > 0 else 1
         tt = np.zeros(max(1, cap))
         tf = np.zeros(max(1, cap))
         res = A.sabr_anneal_result(_dptr(best), 0.0, 0, _dptr(tt), _dptr(tf), cap, 0)

@@ -107,6 +107,43 @@ struct Xoshiro {
     static SABR_HD double top53(uint64_t n) { return static_cast<double>(n & ~0x7ffull); }
     // the uniform() that the next draw would return, without drawing it
     SABR_HD double peek_uniform() const { return top53(rotl64c<23>(s0 + s3) + s0) * 0x1.0p-64; }
+    // the next draw's 53 significant bits in place: uniform() = peek_bits() * 2^-64 exactly
+    SABR_HD uint64_t peek_bits() const { return (rotl64c<23>(s0 + s3) + s0) & ~0x7ffull; }
+    // advance() when p, in place and without selects: the eight 32-bit words
+    // are updated by predicated instructions in an order that reads every old
+    // word before it is overwritten (s1 first, s0 from s3 ^ s1 kept aside);
+    // the select form (a copy advanced, then chosen) costs eight more ALU ops.
+    SABR_HD void advance_if(bool p) {
+#ifdef __CUDA_ARCH__
+        uint32_t a0 = static_cast<uint32_t>(s0), b0 = static_cast<uint32_t>(s0 >> 32);
+        uint32_t a1 = static_cast<uint32_t>(s1), b1 = static_cast<uint32_t>(s1 >> 32);
+        uint32_t a2 = static_cast<uint32_t>(s2), b2 = static_cast<uint32_t>(s2 >> 32);
+        uint32_t a3 = static_cast<uint32_t>(s3), b3 = static_cast<uint32_t>(s3 >> 32);
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 tl, th, xl, xh;\n\t"
+            "setp.ne.u32 q, %8, 0;\n\t"
+            "shl.b32 tl, %2, 17;\n\t"                 // t = s1 << 17
+            "shf.l.clamp.b32 th, %2, %3, 17;\n\t"
+            "xor.b32 xl, %6, %2;\n\t"                  // x = s3 ^ s1
+            "xor.b32 xh, %7, %3;\n\t"
+            "@q lop3.b32 %2, %2, %4, %0, 0x96;\n\t"  // s1 ^= s2 ^ s0
+            "@q lop3.b32 %3, %3, %5, %1, 0x96;\n\t"
+            "@q lop3.b32 %4, %4, %0, tl, 0x96;\n\t"  // s2 ^= s0 ^ t
+            "@q lop3.b32 %5, %5, %1, th, 0x96;\n\t"
+            "@q xor.b32 %0, %0, xl;\n\t"              // s0 ^= s3 ^ s1
+            "@q xor.b32 %1, %1, xh;\n\t"
+            "@q shf.l.wrap.b32 %6, xl, xh, 13;\n\t"   // s3 = rotl(s3 ^ s1, 45)
+            "@q shf.l.wrap.b32 %7, xh, xl, 13;\n\t"
+            "}"
+            : "+r"(a0), "+r"(b0), "+r"(a1), "+r"(b1), "+r"(a2), "+r"(b2), "+r"(a3), "+r"(b3)
+            : "r"(static_cast<uint32_t>(p)));
+        s0 = (static_cast<uint64_t>(b0) << 32) | a0;
+        s1 = (static_cast<uint64_t>(b1) << 32) | a1;
+        s2 = (static_cast<uint64_t>(b2) << 32) | a2;
+        s3 = (static_cast<uint64_t>(b3) << 32) | a3;
+#else
+        if (p) advance();
+#endif
+    }
     // uniform(), rng.hpp:42: (next() >> 11) * 2^-53 (exact conversion)
     SABR_HD double uniform() { return top53(next()) * 0x1.0p-64; }
     // 2*uniform() - 1 (annealer.cpp:66) in one exact FMA: (n >> 11) * 2^-52
@@ -186,8 +223,16 @@ SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, dou
 // long double (kernels_mc.cu: exp_table_host()).
 constexpr int kExpTableSize = 128;
 
+// The table replicated across the shared-memory bank groups: entry i of copy
+// c at [kExpRep * i + c], and a lane reads copy (lane & 7) (the caller passes
+// tab + (lane & 7) and STRIDE = kExpRep).  The eight lanes of a quarter-warp,
+// one LDS.128 wavefront, then never meet in a bank: random arguments no
+// longer serialise the lookup (8.9-way conflicts on the shared table, ncu).
+constexpr int kExpRep = 8;
+
 // exp_tab without the saturation test: valid for |x| <= 700 only (callers
 // that can bound the argument on the host use it and save the compare/select).
+template <int STRIDE = 1>
 SABR_D double exp_tab_unsat(double x, const double2* __restrict__ tab) {
     constexpr double kInvLn2N = 0x1.71547652b82fep7;  // 128 / ln 2
     constexpr double kShift = 0x1.8p52;
@@ -202,17 +247,55 @@ SABR_D double exp_tab_unsat(double x, const double2* __restrict__ tab) {
     const double r2 = r * r;
     const double q = fma(fma(r, 1.0 / 120, 1.0 / 24), r2, fma(r, 1.0 / 6, 0.5));
     const double p = fma(q, r2, r);
-    const double2 t = tab[k & 127];
+    const double2 t = tab[(k & 127) * STRIDE];
     const double v = t.x + fma(t.x, p, t.y);
     // scale by 2^(k >> 7): add to the exponent field (result stays normal for |x| <= 700)
     return __hiloint2double(__double2hiint(v) + ((k >> 7) << 20), __double2loint(v));
 }
 
+template <int STRIDE = 1>
 SABR_D double exp_tab(double x, const double2* __restrict__ tab) {
-    const double res = exp_tab_unsat(x, tab);
+    const double res = exp_tab_unsat<STRIDE>(x, tab);
     // NaN fails the test and flows through the arithmetic into res
     const double sat = x > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0;
     return fabs(x) > 700.0 ? sat : res;
+}
+
+// ----------------------------------------------------------- Metropolis ---
+// annealer.cpp:125-126: accept iff fy <= fx || u < exp(-(fy - fx) / T), with
+// u = uniform() drawn only when fy > fx.  With tau = -ln u the test is
+// q < tau, q = (fy - fx) / T, and tau depends only on the chain's stream, not
+// on the objective, so it is computed off the critical path in FP32 (one
+// I2F.F32, one MUFU.LG2) and the comparison certified with a margin:
+//   |tau_f - tau| <= 2^-18 + 2^-22 tau (2^-24 relative rounding of the 53-bit
+//   draw, lg2.approx's 2^-22 absolute error, the FADD/FMUL roundings),
+//   |q_f - q| <= 2^-23 q (q_f = RN_f32((fy - fx) * RN(1/T)), RN(1/T) 1 ulp),
+// so |q_f - tau_f| > 2^-15 (1 + tau_f) decides q < tau exactly, and with
+// margin ~1.5e-5 relative the glibc exp's own rounding cannot flip it either.
+// Otherwise (probability ~3e-5 per uphill step) the caller decides with
+// metropolis_exact: the reference's division and a libdevice exp.  tau_f is
+// capped at 745: u = 0 (m = 0) accepts iff exp(-q) > 0, i.e. q < 745.13..., and
+// the cap's margin band sends q near 745 to the exact test.  q = +inf (fy =
+// +inf) rejects; q = NaN cannot occur uphill (fy > fx excludes fx = +inf).
+SABR_D float neg_log_uniform(uint64_t m) {  // m = peek_bits(): u = m * 2^-64
+    const float mf = __ull2float_rn(m);
+    float lg;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(mf));  // -inf for m = 0
+    return fminf((64.0f - lg) * 0.693147182f, 745.0f);
+}
+struct MetroFast {
+    bool accept, unsure;
+};
+SABR_D MetroFast metropolis_fast(double fy, double fx, double inv_temp, float tau) {
+    const bool up = !(fy <= fx);
+    const float qf = __double2float_rn((fy - fx) * inv_temp);
+    const float diff = qf - tau;
+    const bool clear = fabsf(diff) > fmaf(tau, 0x1p-15f, 0x1p-15f);
+    return MetroFast{!up || (qf < tau), up && !clear};
+}
+SABR_D bool metropolis_exact(double fy, double fx, double temp, uint64_t m) {
+    const double u = static_cast<double>(m) * 0x1.0p-64;
+    return u < exp(-((fy - fx) / temp));
 }
 
 // ---------------------------------------------------- table log / sqrt ---

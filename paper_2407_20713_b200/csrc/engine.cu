@@ -219,7 +219,8 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
                      const std::vector<double>& hi, const std::vector<double>& start_full,
                      const sabr_schedule& sch, bool start_ok, int64_t records,
                      const StartFn& start, const LevelFn& level_fn, int builtin, int pred,
-                     bool use_peer = false, const RunAllFn& run_all = nullptr) {
+                     bool use_peer = false, const RunAllFn& run_all = nullptr,
+                     bool skips_infeasible = false) {
     validate_schedule(sch);
     // SearchSpace::validate, annealer.cpp:48-58
     if (free_mask == 0) fail(SABR_E_DOMAIN, "SearchSpace: bounds must be nonempty and equal-sized");
@@ -232,7 +233,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     if (pred == SABR_PRED_SUM_LE_1 && !(start_full[0] + start_full[1] <= 1.0)) feasible = false;
     if (!feasible || !start_ok) fail(SABR_E_DOMAIN, "annealer: start point is infeasible");
 
-    const std::vector<double> temps = temperatures(sch);
+    const std::vector<double> temps = temperatures(sch, pred == SABR_PRED_NONE && !skips_infeasible ? level_cap_all_evals(sch) : -1);
     const int64_t L = static_cast<int64_t>(temps.size());
     const int64_t n_chains = static_cast<int64_t>(sch.workers) * sch.groups;
     const int64_t begin = ctx->rank * n_chains / ctx->nranks;
@@ -288,12 +289,34 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
 
     // fused peer exchange (all ranks decide alike: every rank has chains iff n_chains >= nranks)
     const bool peer = ctx->peer && ctx->nranks > 1 && n_chains >= ctx->nranks && use_peer;
+    if (ctx->nranks > 1) {
+        // Every rank must run the same exchange mode: a rank on the peer
+        // mailboxes and a rank in the per-level all-gather would wait on each
+        // other.  One all-gather of the mode byte over the transport, which
+        // doubles as a barrier before level 0, so the mailbox timeout below
+        // starts with every rank inside the run.
+        const uint64_t mine = peer ? 1u : 0u;
+        auto* dsend = static_cast<uint64_t*>(dev_buf(ctx, "mode_send", sizeof(uint64_t)));
+        auto* drecv = static_cast<uint64_t*>(dev_buf(ctx, "mode_recv", sizeof(uint64_t) * ctx->nranks));
+        check_cuda(cudaMemcpyAsync(dsend, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream), "H2D mode");
+        allgather(ctx, dsend, drecv, sizeof(uint64_t));
+        std::vector<uint64_t> modes(ctx->nranks);
+        check_cuda(cudaMemcpyAsync(modes.data(), drecv, sizeof(uint64_t) * ctx->nranks, cudaMemcpyDeviceToHost,
+                                   ctx->stream), "D2H modes");
+        sync(ctx);
+        for (int r = 0; r < ctx->nranks; ++r)
+            if (modes[r] != mine)
+                fail(SABR_E_INVALID, "exchange mode differs between ranks (enable/disable the peer exchange on "
+                                     "every rank)");
+    }
     if (peer) {
         a.peer_boxes = ctx->peer_boxes;
         a.my_rank = ctx->rank;
         a.epoch_base = ctx->peer_epoch;
         a.peer_error = ctx->peer_error;
         ctx->peer_epoch += static_cast<unsigned long long>(L);
+        // a timeout of an earlier run must not fail this one
+        check_cuda(cudaMemsetAsync(ctx->peer_error, 0, sizeof(int), ctx->stream), "memset peer error");
     }
 
     Timer timer(ctx);
@@ -1176,9 +1199,23 @@ SABR_API sabr_status sabr_ctx_enable_peer_exchange(sabr_ctx* ctx) {
     });
 }
 
+// Collective, like enable: a barrier over the transport (no rank can still be
+// storing into a mailbox: runs are synchronous calls and every rank reaches
+// this point), then the peers' mappings are closed and the own mailbox freed.
 SABR_API sabr_status sabr_ctx_disable_peer_exchange(sabr_ctx* ctx) {
     return guarded([&] {
         CtxLock l(ctx);
+        if (!ctx->peer) return;
+        auto* dsend = static_cast<unsigned char*>(dev_buf(ctx, "peer_h_send", sizeof(cudaIpcMemHandle_t)));
+        auto* drecv = static_cast<unsigned char*>(
+            dev_buf(ctx, "peer_h_recv", sizeof(cudaIpcMemHandle_t) * ctx->nranks));
+        allgather(ctx, dsend, drecv, sizeof(cudaIpcMemHandle_t));
+        sync(ctx);
+        for (void* p : ctx->peer_opened) cudaIpcCloseMemHandle(p);
+        ctx->peer_opened.clear();
+        if (ctx->peer_box) cudaFree(ctx->peer_box);
+        ctx->peer_box = nullptr;
+        ctx->peer_boxes = nullptr;
         ctx->peer = false;
     });
 }
@@ -1452,7 +1489,8 @@ SABR_API sabr_status sabr_calibrate_case2_formula(sabr_ctx* ctx, const sabr_surf
                 [&](const SaLevelArgs& a, int64_t level, double temp) {
                     return launch_c2f_level(v, a, level, temp, s);
                 },
-                0, SABR_PRED_NONE);
+                0, SABR_PRED_NONE, /*use_peer=*/false, nullptr,
+                /*skips_infeasible=*/true);  // case2_feasible inside the level kernel
             best_full = r.best_full;
             rep.final_cost = r.best_value;
             rep.evals = r.evals;

@@ -132,10 +132,24 @@ inline void validate_plan(const sabr_plan& p) {
 }
 
 // The temperatures of annealer.cpp:99-100 (repeated product, not t0*c^k).
-inline std::vector<double> temperatures(const sabr_schedule& s) {
+// The reference's level loop also stops once evals >= max_evals; when every
+// step is an evaluation (no feasibility predicate) a level adds at least
+// min(n_chains, remaining) evals, so at most ceil((max_evals - 1) / n_chains)
+// + 1 levels can run and the list is cut there (a valid but extreme cooling
+// such as 1 - 1e-10 would otherwise build ~1e11 temperatures).  max_levels < 0:
+// no cut (with a predicate, infeasible steps do not count).
+inline std::vector<double> temperatures(const sabr_schedule& s, int64_t max_levels = -1) {
     std::vector<double> t;
-    for (double temp = s.t0; temp >= s.t_min; temp *= s.cooling) t.push_back(temp);
+    for (double temp = s.t0; temp >= s.t_min; temp *= s.cooling) {
+        if (max_levels >= 0 && static_cast<int64_t>(t.size()) >= max_levels) break;
+        t.push_back(temp);
+    }
     return t;
+}
+
+inline int64_t level_cap_all_evals(const sabr_schedule& s) {
+    const int64_t n = static_cast<int64_t>(s.workers) * s.groups;
+    return (s.max_evals - 1 + n - 1) / n + 1;
 }
 
 // ------------------------------------------------------------ ParamSpace ---

@@ -102,12 +102,12 @@ __device__ Grid stage_grid(const SurfaceView& sv, unsigned char* smem) {
 // f^(1-beta) = exp((1-beta) ln f) with ln f carried in double-double, so the
 // result is as accurate as a correctly rounded exp (pow in analytics.cpp:191).
 // SAT = false: |(1-beta) ln f| <= 700 is guaranteed by the host (FAST kernels).
-template <bool SAT = true>
+template <bool SAT = true, int STRIDE = 1>
 __device__ __forceinline__ double pow_fwd(double omb, double lnf_hi, double lnf_lo,
                                           const double2* tab) {
     const double y = omb * lnf_hi;
     const double err = fma(omb, lnf_hi, -y) + omb * lnf_lo;
-    const double e = SAT ? exp_tab(y, tab) : exp_tab_unsat(y, tab);
+    const double e = SAT ? exp_tab<STRIDE>(y, tab) : exp_tab_unsat<STRIDE>(y, tab);
     return fma(e, err, e);
 }
 
@@ -339,13 +339,13 @@ __device__ __forceinline__ StaticSlice static_slice(const PGrid& g) {
     return StaticSlice{g.lnf_hi[0], g.lnf_lo[0], g.T[0], g.rec + g.p0[0], g.nq[0]};
 }
 
-template <int C, int DIMF, bool FAST>
+template <int C, int DIMF, bool FAST, int STRIDE = 1>
 __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const StaticSlice& sl,
                                               const double2* tab, double (&out)[C]) {
     QuadTerms t[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const double pw = pow_fwd<!FAST>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
+        const double pw = pow_fwd<!FAST, STRIDE>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
         t[c] = quad_terms(static_terms(v[c][0], v[c][1], v[c][2], v[c][3], pw, sl.T));
     }
     quad_cost_n<C>(t, sl.rec, sl.nq, out);
@@ -470,12 +470,12 @@ __device__ __forceinline__ QrSlice qr_slice(const QGrid& g) {
     return QrSlice{g.lnf_hi[0], g.lnf_lo[0], g.T[0], load_qr(g.R)};
 }
 
-template <int C, int DIMF, bool FAST>
+template <int C, int DIMF, bool FAST, int STRIDE = 1>
 __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const QrSlice& sl,
                                               const double2* tab, double (&out)[C]) {
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const double pw = pow_fwd<!FAST>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
+        const double pw = pow_fwd<!FAST, STRIDE>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
         out[c] = qr_cost(static_qterms(v[c], pw, sl.T), sl.f);
     }
 }
@@ -668,13 +668,17 @@ __device__ __noinline__ void peer_exchange_and_merge(const SaLevelArgs& a, const
     const int par = static_cast<int>(epoch & 1ull);
     for (int r = 0; r < a.nranks; ++r) a.peer_boxes[r]->rec[par][a.my_rank] = out;
     __threadfence_system();
+    // system-scope atomics: the mailboxes are written by other GPUs
     for (int r = 0; r < a.nranks; ++r)
-        atomicExch(&a.peer_boxes[r]->epoch[par][a.my_rank], epoch);
+        atomicExch_system(&a.peer_boxes[r]->epoch[par][a.my_rank], epoch);
     PeerMailbox* own = a.peer_boxes[a.my_rank];
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int r = 0; r < a.nranks; ++r) {
-        while (atomicAdd(&own->epoch[par][r], 0ull) < epoch) {
+        for (;;) {
+            unsigned long long seen;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(seen) : "l"(&own->epoch[par][r]) : "memory");
+            if (seen >= epoch) break;
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             if (t - t0 > 20000000000ull) {  // 20 s
@@ -867,9 +871,10 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
             // size of the reference's own exp rounding).
             bool accept = fy <= fx;
             if (!accept) {
-                const double q = (fy - fx) * inv_temp;
-                const double u = rng.uniform();
-                accept = ALLFREE ? (q <= 700.0 && u < exp_tab_unsat(-q, tab_s)) : u < exp_tab(-q, tab_s);
+                const uint64_t m = rng.peek_bits();
+                rng.advance();
+                const MetroFast mf = metropolis_fast(fy, fx, inv_temp, neg_log_uniform(m));
+                accept = mf.unsure ? metropolis_exact(fy, fx, temp, m) : mf.accept;
             }
             if (accept) {
 #pragma unroll
@@ -928,7 +933,8 @@ constexpr int kMaxPwSlices = 64;
 // Shared by the per-level kernel and the single-CTA persistent kernel.
 template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT>
 __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const ObjGrid<GK>& g,
-                                                 const double2* tab_s, const double* pw_fixed,
+                                                 const double2* tab_s, const double2* tab_lane,
+                                                 const double* pw_fixed,
                                                  const sabr_sa_state* st, const double temp,
                                                  const double inv_temp, const bool (&active)[C],
                                                  const int64_t (&chain)[C], Xoshiro (&rng)[C],
@@ -973,28 +979,45 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
                         y[c][i] = x[c][i];
                 }
             }
+            // the Metropolis draw of this step (used only when fy > fx) and
+            // its -ln u: they depend on the stream alone, so they are ready
+            // before the objective is (metropolis_fast)
+            uint64_t mbits[C];
+            float tau[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                mbits[c] = rng[c].peek_bits();
+                tau[c] = neg_log_uniform(mbits[c]);
+            }
             double fy[C];
-            if constexpr (KIND == OBJ_STATIC) static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
-            else if constexpr (GK == kGridQR) case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
+            if constexpr (KIND == OBJ_STATIC) {
+                if (tab_lane) static_cost_n<C, DIMF, ALLFREE, kExpRep>(y, sl, tab_lane, fy);
+                else static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
+            } else if constexpr (GK == kGridQR) case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
             else case1_cost_n<C, DIMF>(y, g, fy);
-            // Metropolis (annealer.cpp:125-126) without a branch, so the
-            // chains' exp chains interleave: exp(-(fy - fx)/T) and the
-            // candidate uniform are computed for every chain; the uniform's
-            // draw is committed (the stream advanced) only when fy > fx, as
-            // the reference draws it.  (fy - fx) / T as in sa_level_kernel.
+            // Metropolis (annealer.cpp:125-126) without a branch: the FP32
+            // certificate decides (metropolis_fast); the draw is committed
+            // (the stream advanced) only when fy > fx, as the reference draws
+            // it.  The rare undecided comparison takes the exact test, whose
+            // verdict goes back into tau (+inf: accept, -inf: reject), so the
+            // decision stays one FP32 compare after the rare branch and no
+            // predicate lives across it.
+            bool unsure = false;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 if (isnan(fy[c])) fy[c] = CUDART_INF;
-                const bool up = !(fy[c] <= fx[c]);
-                const double q = (fy[c] - fx[c]) * inv_temp;
-                const double u = rng[c].peek_uniform();
-                Xoshiro adv = rng[c];
-                adv.advance();
-                if (up) rng[c] = adv;
-                // exp_tab(-q) is 0 for q > 700 (and NaN for NaN q): u < 0 is
-                // false.  Non-short-circuit ops: no branch around the exp.
-                const double ex = ALLFREE ? exp_tab_unsat(-q, tab_s) : exp_tab(-q, tab_s);
-                const bool accept = ALLFREE ? (!up | ((q <= 700.0) & (u < ex))) : (!up | (u < ex));
+                unsure |= metropolis_fast(fy[c], fx[c], inv_temp, tau[c]).unsure;
+                rng[c].advance_if(!(fy[c] <= fx[c]));
+            }
+            if (unsure) {
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (metropolis_fast(fy[c], fx[c], inv_temp, tau[c]).unsure)
+                        tau[c] = metropolis_exact(fy[c], fx[c], temp, mbits[c]) ? CUDART_INF_F : -CUDART_INF_F;
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const bool accept = metropolis_fast(fy[c], fx[c], inv_temp, tau[c]).accept;
                 const bool better = accept && fy[c] < bv[c];
 #pragma unroll
                 for (int i = 0; i < DIMF; ++i) x[c][i] = accept ? y[c][i] : x[c][i];
@@ -1039,10 +1062,13 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
     constexpr int NT = level_nt<C>();
+    // the static objective's pow reads the bank-replicated exp table
+    constexpr bool kRep = KIND == OBJ_STATIC && GK == kGridQR;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
     __shared__ sabr_level_record rec;
     __shared__ double2 tab_s[kExpTableSize];
+    __shared__ double2 tabr_s[kRep ? kExpTableSize * kExpRep : 1];
     __shared__ double bp_s[C][DIMF][NT];
 
     sabr_sa_state* st = a.state;
@@ -1053,9 +1079,12 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     // previous level is read before pdl_wait().
     pdl_trigger();
     stage_exp(sv, tab_s);
+    if constexpr (kRep)
+        for (int i = threadIdx.x; i < kExpTableSize * kExpRep; i += NT) tabr_s[i] = sv.exptab[i / kExpRep];
     ObjGrid<GK> g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
+    const double2* tab_lane = kRep ? tabr_s + (threadIdx.x & (kExpRep - 1)) : nullptr;
 
     bool active[C];
     int64_t chain[C];
@@ -1081,8 +1110,8 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
             pw_fixed = pw_s;
         }
     }
-    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, pw_fixed, st, temp, inv_temp, active, chain,
-                                                     rng, bp_s, rs, rec);
+    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, tab_lane, pw_fixed, st, temp, inv_temp, active,
+                                                     chain, rng, bp_s, rs, rec);
     if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
     reduce_block_records<NT, DIMF>(rs, a, level);
 }
@@ -1136,8 +1165,8 @@ __global__ void __launch_bounds__(kLevelThreads / C, 1)
 #pragma unroll
         for (int c = 0; c < C; ++c)
             rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
-        run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, pw_fixed, st, temp, inv_temp, active, chain,
-                                                         rng, bp_s, rs, rec);
+        run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, nullptr, pw_fixed, st, temp, inv_temp,
+                                                         active, chain, rng, bp_s, rs, rec);
         if (threadIdx.x == 0) {
             sabr_level_record out;
             const bool e_ok = rs.e_win.i != LLONG_MAX, b_ok = rs.b_win.i != LLONG_MAX;
@@ -1667,7 +1696,7 @@ cudaError_t launch_sa_start(int kind, const SurfaceView& sv, const SaLevelArgs& 
 
 namespace {
 __global__ void peer_hello_kernel(PeerMailbox* const* boxes, int nranks, int my_rank, unsigned long long magic) {
-    for (int r = 0; r < nranks; ++r) atomicExch(&boxes[r]->hello[my_rank], magic);
+    for (int r = 0; r < nranks; ++r) atomicExch_system(&boxes[r]->hello[my_rank], magic);
     __threadfence_system();
 }
 }  // namespace

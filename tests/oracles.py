@@ -183,7 +183,7 @@ class Ref:
 
     def _anneal(self, fn, dim, schedule, *args):
         best = np.zeros(max(1, dim))
-        cap = n_levels(schedule)
+        cap = n_levels(schedule, all_evals=False)
         tt, tf = np.zeros(max(1, cap)), np.zeros(max(1, cap))
         res = A.sabr_anneal_result(_dptr(best), 0.0, 0, _dptr(tt), _dptr(tf), cap, 0)
         self._check(fn(*args, C.byref(res)))
@@ -310,7 +310,7 @@ class Restate:
 
     def _anneal(self, fn, dim, schedule, *args):
         best = np.zeros(max(1, dim))
-        cap = n_levels(schedule)
+        cap = n_levels(schedule, all_evals=False)
         tt, tf = np.zeros(max(1, cap)), np.zeros(max(1, cap))
         res = A.sabr_anneal_result(_dptr(best), 0.0, 0, _dptr(tt), _dptr(tf), cap, 0)
         self._check(fn(*args, C.byref(res)))
