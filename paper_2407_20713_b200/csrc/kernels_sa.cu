@@ -873,8 +873,10 @@ __global__ void __launch_bounds__(kLevelThreads, kLevelMinCtas)
             if (!accept) {
                 const uint64_t m = rng.peek_bits();
                 rng.advance();
-                const MetroFast mf = metropolis_fast(fy, fx, inv_temp, neg_log_uniform(m));
-                accept = mf.unsure ? metropolis_exact(fy, fx, temp, m) : mf.accept;
+                float tau = neg_log_uniform(m);
+                if (metropolis_fast(fy, fx, inv_temp, tau).unsure)
+                    tau = metropolis_exact(fy, fx, temp, m) ? CUDART_INF_F : -CUDART_INF_F;
+                accept = metropolis_fast(fy, fx, inv_temp, tau).accept;
             }
             if (accept) {
 #pragma unroll
