@@ -674,10 +674,10 @@ __device__ __forceinline__ void case1_series_pair(double x, const double* __rest
     g = horner_s(ser, 2 * PAIR + 1, x);
 }
 
-template <int PAIR>
+template <int PAIR, int STRIDE = 1>
 __device__ __forceinline__ void case1_closed_pair(double x, const double2* __restrict__ tab, double& f,
                                                   double& g) {
-    const double e = exp_tab(-x, tab);
+    const double e = exp_tab<STRIDE>(-x, tab);
     const double x2 = SABR_MUL(x, x);
     if constexpr (PAIR == 0) {
         const double c6 = 6.0 * fast_rcp(SABR_MUL(x2, x));
@@ -696,7 +696,7 @@ __device__ __forceinline__ void case1_closed_pair(double x, const double2* __res
 // same branch (the rule late in a schedule, when the chains cluster), their
 // evaluations share one branch body and interleave (C-fold ILP); mixed
 // threads evaluate chain by chain.  Per-chain results do not depend on C.
-template <int PAIR, int C>
+template <int PAIR, int C, int STRIDE = 1>
 __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
                                              const double2* __restrict__ tab, double (&f)[C], double (&g)[C]) {
     constexpr double kXSwitch = 0.25;  // analytics.cpp:21
@@ -711,12 +711,12 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
         for (int c = 0; c < C; ++c) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
     } else if (all_closed) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) case1_closed_pair<PAIR>(x[c], tab, f[c], g[c]);
+        for (int c = 0; c < C; ++c) case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
     } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (x[c] < kXSwitch) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
-            else case1_closed_pair<PAIR>(x[c], tab, f[c], g[c]);
+            else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
         }
     }
 }

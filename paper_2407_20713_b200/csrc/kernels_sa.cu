@@ -483,9 +483,11 @@ __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const 
 // pw_fixed: when beta is not searched, f_i^(1-beta) per slice, computed once
 // per CTA with the same pow_fwd (so the values are the ones each chain would
 // compute); nullptr when beta is free.
-template <int C, int DIMF>
+template <int C, int DIMF, int STRIDE = 1>
 __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const QGrid& g,
-                                             double (&out)[C], const double* pw_fixed = nullptr) {
+                                             double (&out)[C], const double* pw_fixed = nullptr,
+                                             const double2* tab = nullptr) {
+    if (STRIDE == 1) tab = g.tab;
 #pragma unroll
     for (int c = 0; c < C; ++c) out[c] = 0.0;
     for (int i = 0; i < g.ns; ++i) {
@@ -498,12 +500,12 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
             xb[c] = SABR_MUL(SABR_MUL(2.0, v[c][5]), T);
             xab[c] = SABR_MUL(SABR_ADD(v[c][4], v[c][5]), T);
         }
-        case1_pair_n<0, C>(xb, g.ser, g.tab, f1, f2);
-        case1_pair_n<1, C>(xab, g.ser, g.tab, g1, g2);
+        case1_pair_n<0, C, STRIDE>(xb, g.ser, tab, f1, f2);
+        case1_pair_n<1, C, STRIDE>(xab, g.ser, tab, g1, g2);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const double nn = SABR_MUL(v[c][3], v[c][3]), nr = SABR_MUL(v[c][3], v[c][2]);
-            const double pw = pw_fixed ? pw_fixed[i] : pow_fwd(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            const double pw = pw_fixed ? pw_fixed[i] : pow_fwd<true, STRIDE>(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], tab);
             QuadTerms t;
             dynamic_quad_terms(SABR_MUL(nn, f1[c]), SABR_MUL(nn, f2[c]), SABR_MUL(nr, g1[c]),
                                SABR_MUL(SABR_MUL(nr, nr), g2[c]), v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
@@ -928,6 +930,10 @@ constexpr int level_nt() { return C == 3 ? 32 : kLevelThreads / C; }
 template <int C>
 constexpr int level_min_ctas() { return C == 3 ? 8 : kPairMinCtas; }
 constexpr int kMaxPwSlices = 64;
+// copies of the bank-replicated exp table (device_common.cuh: kExpRep) per
+// objective in the C-chain level kernel
+template <int KIND>
+constexpr int rep_copies() { return KIND == OBJ_STATIC ? kExpRep : 4; }
 
 // The chains of one CTA for one level (annealer.cpp:107-139) and the CTA's
 // level-end arg-min (annealer.cpp:141-159): on return (all threads) rs holds
@@ -993,9 +999,12 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             }
             double fy[C];
             if constexpr (KIND == OBJ_STATIC) {
-                if (tab_lane) static_cost_n<C, DIMF, ALLFREE, kExpRep>(y, sl, tab_lane, fy);
+                if (tab_lane) static_cost_n<C, DIMF, ALLFREE, rep_copies<KIND>()>(y, sl, tab_lane, fy);
                 else static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
-            } else if constexpr (GK == kGridQR) case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
+            } else if constexpr (GK == kGridQR) {
+                if (tab_lane) case1_cost_n<C, DIMF, rep_copies<KIND>()>(y, g, fy, pw_fixed, tab_lane);
+                else case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
+            }
             else case1_cost_n<C, DIMF>(y, g, fy);
             // Metropolis (annealer.cpp:125-126) without a branch: the FP32
             // certificate decides (metropolis_fast); the draw is committed
@@ -1065,12 +1074,17 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
                           const int64_t level, const double temp, const double inv_temp) {
     constexpr int NT = level_nt<C>();
     // the static objective's pow reads the bank-replicated exp table
-    constexpr bool kRep = KIND == OBJ_STATIC && GK == kGridQR;
+    // (Case I: 8 copies would take 22 KB per CTA and push its 1563 one-warp
+    // CTAs out of one wave; 4 copies halve the conflicts, 1.93x the ideal
+    // wavefronts, but the kernel is bound by FP64 dependency latency and ran
+    // no faster: ncu r02, 649 vs 656 us per level, so Case I keeps one copy)
+    constexpr bool kRep = GK == kGridQR && KIND == OBJ_STATIC;
+    constexpr int kRepN = rep_copies<KIND>();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
     __shared__ sabr_level_record rec;
     __shared__ double2 tab_s[kExpTableSize];
-    __shared__ double2 tabr_s[kRep ? kExpTableSize * kExpRep : 1];
+    __shared__ double2 tabr_s[kRep ? kExpTableSize * kRepN : 1];
     __shared__ double bp_s[C][DIMF][NT];
 
     sabr_sa_state* st = a.state;
@@ -1082,11 +1096,11 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     pdl_trigger();
     stage_exp(sv, tab_s);
     if constexpr (kRep)
-        for (int i = threadIdx.x; i < kExpTableSize * kExpRep; i += NT) tabr_s[i] = sv.exptab[i / kExpRep];
+        for (int i = threadIdx.x; i < kExpTableSize * kRepN; i += NT) tabr_s[i] = sv.exptab[i / kRepN];
     ObjGrid<GK> g = stage_obj<GK>(sv, smem);
     __syncthreads();
     g.tab = tab_s;
-    const double2* tab_lane = kRep ? tabr_s + (threadIdx.x & (kExpRep - 1)) : nullptr;
+    const double2* tab_lane = kRep ? tabr_s + (threadIdx.x & (kRepN - 1)) : nullptr;
 
     bool active[C];
     int64_t chain[C];
