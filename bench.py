@@ -366,6 +366,13 @@ def run_ours(args):
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(fx)
+        c1 = line.get("secondary", {}).get("c1_static_calibration")
+        m = line["cpu_baseline"].get("matrix")
+        if c1 and m:
+            # C1 is the one config whose whole reference run is short: same-config wall-time ratio
+            ref_s = m[f"threads_{line['cpu_baseline']['cores']}"]["c1_static_calibration_s"]
+            c1["reference_s_all_threads"] = ref_s
+            c1["speedup_vs_reference_same_config"] = ref_s / c1["value"]
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -505,24 +512,86 @@ def secondary(eng, torch, dev, stream):
     return out
 
 
+def host_info():
+    """CPU model, logical CPUs and glibc of the host running the CPU arms."""
+    import platform
+
+    model = platform.processor() or "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "glibc": "-".join(platform.libc_ver())}
+
+
 def cpu_baseline(fx):
-    """The compiled reference (oracle/_ref) on the host cores, bounded sample."""
+    """The compiled reference (oracle/_ref) on the host cores: the headline
+    C2 sample at all threads (the line's cpu_baseline), plus the BASELINE.md
+    section 3 matrix - C1 (whole run), C2, C3, C4 and C5 at 1 thread and at all
+    threads, each a bounded sample (about 20 s in total)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracles import Ref, have_ref
+
+    import paper_2407_20713_b200 as pkg
 
     if not have_ref():
         return {"value": None, "unit": "cost-evals/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
     ref = Ref()
     threads = ref.max_threads()
+
+    def timed(fn):
+        t0 = time.perf_counter()
+        out = fn()
+        return out, time.perf_counter() - t0
+
     sch = c2_schedule(1, max_evals=2 * 10 ** 7 + 1)
     sch.omp_threads = threads
-    t0 = time.perf_counter()
-    rep = ref.calibrate_static_T1(fx, 0, None, sch, None)
-    secs = time.perf_counter() - t0
-    return {"value": (rep.evals - 1) / secs, "unit": "cost-evals/s", "cores": threads, "kind": "reference",
+    rep, secs = timed(lambda: ref.calibrate_static_T1(fx, 0, None, sch, None))
+    line = {"value": (rep.evals - 1) / secs, "unit": "cost-evals/s", "cores": threads, "kind": "reference",
             "sample": f"calibrate_static_T1(eurusd slice 0), C2 schedule capped at max_evals=2e7 "
                       f"(first 2 levels, {rep.evals - 1} evals, {secs:.1f} s)"}
+    eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
+    matrix = {}
+    for n in sorted({1, threads}):
+        row = {}
+        # C1: the reference's own CPU-sized case, the whole acceptance-schedule run
+        s1 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=1)
+        s1.omp_threads = n
+        r, t = timed(lambda: ref.calibrate_static_T1(eq, 0, None, s1, None))
+        row["c1_static_calibration_s"] = t
+        row["c1_cost_evals_per_s"] = (r.evals - 1) / t
+        # C2: the C2 schedule on one EUR/USD slice, first level (1e7 evals; 1e6 at 1 thread)
+        s2 = c2_schedule(1, max_evals=(10 ** 7 if n > 1 else 10 ** 6) + 1)
+        s2.omp_threads = n
+        r, t = timed(lambda: ref.calibrate_static_T1(fx, 0, None, s2, None))
+        row["c2_cost_evals_per_s"] = (r.evals - 1) / t
+        # C3: Case I joint calibration, acceptance schedule, beta = 1 (1e6 evals)
+        s3 = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=1)
+        s3.omp_threads = n
+        r, t = timed(lambda: ref.calibrate_dynamic_case1_T1(fx, None, s3, {"beta": 1.0}))
+        row["c3_cost_evals_per_s"] = (r.evals - 1) / t
+        # C4: one MC cost-eval (case2_mc_cost, 1e5 paths x 250 steps, static dynamics)
+        surf4, _, _, plan4 = c4_setup()
+        plan4.workers = n
+        P4 = np.array([[0.30, 1.0, -0.45, 0.0, 0.0, 0.9, 0.0, 0.0, 0.0, 0.0, 1.0]])
+        _, t = timed(lambda: ref.cost_case2_mc(surf4, P4, plan4))
+        row["c4_path_steps_per_s"] = 1e5 * 250 / t
+        # C5: one MC cost-eval on the 20x30 surface (4096 paths, 13130 steps per path)
+        surf5 = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "synth20x30.csv"))
+        plan5 = pkg.SimulationPlan(num_paths=4096, dt=1 / 250, seed=1, rng="xoshiro")
+        plan5.workers = n
+        P5 = np.array([FX_CASE2 + [5.0]])
+        _, t = timed(lambda: ref.cost_case2_mc(surf5, P5, plan5))
+        row["c5_path_steps_per_s"] = 4096 * 13130 / t
+        matrix[f"threads_{n}"] = row
+    line["matrix"] = matrix
+    line["host"] = host_info()
+    return line
 
 
 def run_reference(args):
