@@ -318,7 +318,8 @@ def run_ours(args):
 
     sec = {}
     if rank == 0 and world == 1 and not args.no_secondary:
-        sec = secondary(eng, torch, dev, stream)
+        mufu = float(np.median([mufu_peak(eng) for _ in range(3)]))
+        sec = secondary(eng, torch, dev, stream, {"fp64_tflops": peak, "mufu_tops": mufu})
 
     line = {
         "metric": "SA cost-evals/s, static Hagan/Obloj (Eq. 7) calibration, EUR/USD surface, 1e5 chains/GPU",
@@ -382,6 +383,24 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def mufu_peak(eng):
+    import ctypes as C
+
+    v = C.c_double()
+    eng._check(eng.lib.sabr_bench_mufu_peak(eng.handle, C.byref(v)))
+    return v.value
+
+
+def pipe_roofline(units_per_s, instr_per_unit, peak_tinstr_per_s, pipe, source):
+    """A kernel's pipe occupancy: units/s x (ncu-counted) lane instructions of
+    that pipe per unit, against the pipe's measured lane-instruction peak."""
+    if not instr_per_unit or not peak_tinstr_per_s:
+        return None
+    a = units_per_s * instr_per_unit / 1e12
+    return {"bound": pipe, "instr_per_unit": instr_per_unit, "achieved": a, "peak": peak_tinstr_per_s,
+            "unit": "T lane-instr/s", "frac": a / peak_tinstr_per_s, "source": source}
+
+
 def fp64_peak(eng):
     import ctypes as C
 
@@ -406,11 +425,21 @@ def fp64_flops_per_eval():
     return {"flops": 1180.0, "source": "SURVEY.md 8(d) estimate (FP64-pipe instr, m=19)"}
 
 
-def secondary(eng, torch, dev, stream):
-    """C4 (MC objective) and C3 (Case I) line items, measured once after a warm-up."""
+def secondary(eng, torch, dev, stream, peaks):
+    """C4 (MC objective) and C3 (Case I) line items, measured once after a warm-up,
+    each with the roofline of its dominant kernel (FP64 pipe, or the XU/MUFU
+    pipe for the FP32 MC path) from profiles/fp64_per_eval.json's ncu counts."""
     import paper_2407_20713_b200 as pkg
 
-    out = {}
+    per = {}
+    pth = os.path.join(ROOT, "profiles", "fp64_per_eval.json")
+    if os.path.exists(pth):
+        with open(pth) as f:
+            per = json.load(f)
+    fp64_lane_peak = peaks["fp64_tflops"] / 2  # DFMA = 2 FLOP: lane instructions / s
+    src = "ncu lane instructions per unit (profiles/fp64_per_eval.json) x kernel units/s / measured pipe peak"
+    out = {"peaks": {"fp64_tflops": peaks["fp64_tflops"], "mufu_tops": peaks["mufu_tops"],
+                     "source": "sabr_bench_fp64_peak / sabr_bench_mufu_peak microbenchmarks (peak.cu), this run"}}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for precision, rng in (("fp64", "xoshiro"), ("fp32", "xoshiro"), ("fp64", "philox")):
         surf, fixed, sch, plan = c4_setup(levels=2)
@@ -436,6 +465,13 @@ def secondary(eng, torch, dev, stream):
             "cost_evals": rep.evals - 1, "levels": 2, "chains": 32, "paths": plan.num_paths,
             "steps_per_path": steps_per_eval, "rng": plan.rng, "precision": precision, "seconds": secs,
             "final_cost": rep.final_cost, "mc_kernel_ms": t.kernel_ms, "mc_launches": t.kernel_launches}
+        kps = t.path_steps / (t.kernel_ms / 1e3)
+        if precision == "fp64":
+            out[key]["roofline"] = pipe_roofline(kps, per.get("c4_fp64_pipe_instr_per_candidate_path_step"),
+                                                 fp64_lane_peak, "fp64", src)
+        else:
+            out[key]["roofline"] = pipe_roofline(kps, per.get("c4_fp32_xu_instr_per_candidate_path_step"),
+                                                 peaks["mufu_tops"], "xu (MUFU)", src)
     # C5: full Case II MC calibration on the 20x30 synthetic surface, one SA step of 2048 chains
     surf, bounds, sch, plan = c5_setup()
     for precision in ("fp64", "fp32"):
@@ -478,6 +514,10 @@ def secondary(eng, torch, dev, stream):
             "metric": f"MC SABR path-steps/s (price_european_batch, 2^24 paths x 124 steps, {precision})",
             "unit": "path-steps/s", "value": ps / secs, "seconds": secs, "price": est[0].value,
             "std_error": est[0].std_error, "paper_gtx470_path_steps_per_s": 2.18e8 if precision == "fp64" else 1.62e9}
+        if precision == "fp64":
+            out["mc_european_pricing"]["roofline"] = pipe_roofline(
+                ps / secs, per.get("mc_single_fp64_pipe_instr_per_path_step"), fp64_lane_peak, "fp64",
+                src + " (whole call: simulate + reduce)")
     # C1 (BASELINE.json configs[0]): the reference's own CPU-sized case, static T_I on one EURO STOXX 50
     # slice with the acceptance schedule (32 chains, 412 levels, 1,000,001 evals): latency-bound on a GPU
     eq = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurostoxx50.csv"))
@@ -509,6 +549,12 @@ def secondary(eng, torch, dev, stream):
     out["c3_case1_calibration"] = {"metric": "SA cost-evals/s, Case I (Eq. 8) joint calibration, EUR/USD, 1e5 chains",
                                    "unit": "cost-evals/s", "value": (rep.evals - 1) / secs, "seconds": secs,
                                    "mean_rel_error": rep.mean_rel_error}
+    if per.get("c3_flops_per_eval"):
+        a = (rep.evals - 1) / secs * per["c3_flops_per_eval"] / 1e12
+        out["c3_case1_calibration"]["roofline"] = {
+            "bound": "fp64", "achieved": a, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+            "frac": a / peaks["fp64_tflops"], "flops_per_eval": per["c3_flops_per_eval"],
+            "source": "ncu DFMA x2 + DADD + DMUL per eval (profiles/fp64_per_eval.json), whole calibration"}
     return out
 
 

@@ -397,6 +397,9 @@ SABR_API sabr_status sabr_surface_csv_read(const char* path, double* spot, doubl
  * (8 independent DFMA chains per thread, 8 CTAs of 256 threads per SM) - the
  * roofline denominator of the FP64-bound kernels. */
 SABR_API sabr_status sabr_bench_fp64_peak(sabr_ctx* ctx, double* tflops);
+/* Diagnostics: measured MUFU (XU pipe) ex2.approx.f32 throughput in 1e12
+ * ops/s - the roofline denominator of the FP32 MC path's transcendentals. */
+SABR_API sabr_status sabr_bench_mufu_peak(sabr_ctx* ctx, double* tops);
 
 /* Black-Scholes call (black_scholes.hpp:7-9), used for the T_II market side. */
 SABR_API sabr_status sabr_black_scholes_call(double spot, double strike, double rate,

@@ -191,7 +191,7 @@ EXPORTS = [
     "sabr_merge_level_records", "sabr_surface_csv_dims", "sabr_surface_csv_read",
     "sabr_black_scholes_call", "sabr_bench_fp64_peak", "sabr_black_scholes_call_batch",
     "sabr_implied_vol_from_price_batch", "sabr_ctx_init_host_exchange", "sabr_ctx_enable_peer_exchange",
-    "sabr_ctx_disable_peer_exchange",
+    "sabr_ctx_disable_peer_exchange", "sabr_bench_mufu_peak",
 ]
 
 # sabr_allgather_fn

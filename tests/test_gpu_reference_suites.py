@@ -23,8 +23,6 @@ unset) and the engine on the B200 (SABR_BACKEND=b200):
   text for every field the engine returns bit-identically (names, parameters,
   evals, seed, maturities, strikes, market quotes), the computed numbers
   (cost, model vols, errors) to 1e-12 relative; wall_seconds excluded."""
-import csv
-import io
 import json
 import os
 import subprocess

@@ -20,12 +20,14 @@ def per(path, prefix, units, pick=-1):
     dmul = g["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"]
     pipe = g.get("smsp__inst_executed_pipe_fp64.sum")  # warp instructions of the FP64 pipe
     warp_inst = g.get("smsp__inst_executed.sum")
+    xu = g.get("smsp__inst_executed_pipe_xu.sum")  # warp instructions of the XU (MUFU) pipe
     return ((2 * dfma + dadd + dmul) / units, (dfma + dadd + dmul) / units,
             g["dram__bytes_read.sum"] + g["dram__bytes_write.sum"], g["gpu__time_duration.sum"],
-            None if pipe is None else 32 * pipe / units, None if warp_inst is None else warp_inst / units)
+            None if pipe is None else 32 * pipe / units, None if warp_inst is None else warp_inst / units,
+            None if xu is None else 32 * xu / units)
 
 
-def main(tag, copy=("sa", "case1", "t2", "t2_cb4", "mc")):
+def main(tag, copy=("sa", "case1", "t2", "t2_fp32", "mc", "c5")):
     src = os.path.join(ROOT, "gpurun_out")
     sa = per(os.path.join(src, "ncu_metrics_sa.csv"), ("sa_level_multi_kernel<0", "sa_level_kernel<0"), 1e7)
     c1 = per(os.path.join(src, "ncu_metrics_case1.csv"), ("sa_level_multi_kernel<1", "sa_level_kernel<1"), 1e7)
@@ -40,7 +42,14 @@ def main(tag, copy=("sa", "case1", "t2", "t2_cb4", "mc")):
          "c3_level_kernel_ns": c1[3],
          "c4_flops_per_candidate_path_step": t2[0], "c4_fp64_instr_per_candidate_path_step": t2[1],
          "c4_dram_bytes_per_launch": t2[2], "c4_mc_kernel_ns": t2[3],
-         "mc_single_flops_per_path_step": mc[0], "mc_single_fp64_instr_per_path_step": mc[1]}
+         "c4_fp64_pipe_instr_per_candidate_path_step": t2[4],
+         "mc_single_flops_per_path_step": mc[0], "mc_single_fp64_instr_per_path_step": mc[1],
+         "mc_single_fp64_pipe_instr_per_path_step": mc[4]}
+    f32 = os.path.join(src, "ncu_metrics_t2_fp32.csv")
+    if os.path.exists(f32):  # the FP32 MC path: MUFU (XU) instructions per candidate-path-step
+        t2f = per(f32, "mc_tile_kernel_f32<8", 32 * 1e5 * 250)
+        d["c4_fp32_xu_instr_per_candidate_path_step"] = t2f[6]
+        d["c4_fp32_mc_kernel_ns"] = t2f[3]
     with open(os.path.join(ROOT, "profiles", "fp64_per_eval.json"), "w") as f:
         json.dump(d, f, indent=1)
     for m in copy:
