@@ -500,8 +500,22 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
             xb[c] = SABR_MUL(SABR_MUL(2.0, v[c][5]), T);
             xab[c] = SABR_MUL(SABR_ADD(v[c][4], v[c][5]), T);
         }
-        case1_pair_n<0, C, STRIDE>(xb, g.ser, tab, f1, f2);
-        case1_pair_n<1, C, STRIDE>(xab, g.ser, tab, g1, g2);
+        // both functional pairs of every chain in the closed-form regime (the
+        // rule on C3's surfaces): one straight-line block, 2C independent
+        // dependency chains (ILP) instead of two branch regions of C
+        bool all_closed = true;
+#pragma unroll
+        for (int c = 0; c < C; ++c) all_closed &= !(xb[c] < 0.25) & !(xab[c] < 0.25);
+        if (all_closed) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                case1_closed_pair<0, STRIDE>(xb[c], tab, f1[c], f2[c]);
+                case1_closed_pair<1, STRIDE>(xab[c], tab, g1[c], g2[c]);
+            }
+        } else {
+            case1_pair_n<0, C, STRIDE>(xb, g.ser, tab, f1, f2);
+            case1_pair_n<1, C, STRIDE>(xab, g.ser, tab, g1, g2);
+        }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const double nn = SABR_MUL(v[c][3], v[c][3]), nr = SABR_MUL(v[c][3], v[c][2]);
