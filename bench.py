@@ -293,7 +293,10 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (the SA level kernel) ----
     peak = float(np.median([fp64_peak(eng) for _ in range(3)]))
     per_eval = fp64_flops_per_eval()
-    avg_launch_s = (kms_tot / klaunch_tot) / 1e3
+    # per-launch time = device time of the timed steps / level launches: the
+    # sampled per-launch events overlap under programmatic dependent launch
+    # (their sum exceeded the step time by ~3%), so the step time bounds it
+    avg_launch_s = t_dev / klaunch_tot
     evals_per_launch = evals_tot / klaunch_tot / world  # this rank's chains
     achieved = evals_per_launch * per_eval["flops"] / avg_launch_s / 1e12
     traffic = per_eval.get("dram_bytes_per_launch")
@@ -351,6 +354,8 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "sa_level_multi_kernel<OBJ_STATIC,4,ALLFREE,QR,3> (3 chains per thread, factored slice cost)",
                      "avg_launch_ms": avg_launch_s * 1e3, "launches": klaunch_tot,
+                     "avg_launch_source": "device time of the timed steps / level-kernel launches (an upper bound: "
+                                          "includes the start/report kernels and launch gaps)",
                      "flops_per_eval": per_eval["flops"], "flops_source": per_eval["source"],
                      "peak_source": "measured in bench.py (sabr_bench_fp64_peak, DFMA microbenchmark); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
