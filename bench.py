@@ -323,6 +323,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_secondary:
         mufu = float(np.median([mufu_peak(eng) for _ in range(3)]))
         sec = secondary(eng, torch, dev, stream, {"fp64_tflops": peak, "mufu_tops": mufu})
+        if args.full_configs:
+            sec.update(full_configs(eng, torch, dev, stream, {"fp64_tflops": peak, "mufu_tops": mufu}))
 
     line = {
         "metric": "SA cost-evals/s, static Hagan/Obloj (Eq. 7) calibration, EUR/USD surface, 1e5 chains/GPU",
@@ -579,6 +581,53 @@ def host_info():
     return {"cpu_model": model, "nproc": os.cpu_count(), "glibc": "-".join(platform.libc_ver())}
 
 
+def full_configs(eng, torch, dev, stream, peaks):
+    """BASELINE configs C4 and C5 at their named sizes (bench.py --full-configs):
+    * C4: calibrate_case2_T2 on the T=1 equity slice with static dynamics, 32
+      chains x 100 steps per level, t_min 1e-7 (all 412 levels), 1e5 paths x
+      250 steps per cost-eval;
+    * C5: one SA step of 125,000 chains (1e6 chains over 8 GPUs, this GPU's
+      share) of the full Case II calibration on the 20x30 surface in the
+      default Case II box (calibration.cpp:46-60), 4096 paths per candidate."""
+    import paper_2407_20713_b200 as pkg
+
+    out = {}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        flush_l2(torch, dev)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return r, e0.elapsed_time(e1) / 1e3
+
+    surf, fixed, _, plan = c4_setup()
+    sch = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=32, t_min=1e-7, seed=1,
+                                max_evals=10 ** 12)
+    rep, secs = timed(lambda: eng.calibrate_case2_T2(surf, None, sch, plan, fixed))
+    t = eng.last_timing()
+    out["c4_full_calibration"] = {
+        "metric": "calibrate_case2_T2 wall time and path-steps/s, C4 (whole calibration: 412 levels, 32 chains, "
+                  "1e5 paths x 250 steps per cost-eval, fp64)",
+        "unit": "path-steps/s", "value": t.path_steps / secs, "seconds": secs, "cost_evals": rep.evals - 1,
+        "path_steps": t.path_steps, "final_cost": rep.final_cost, "params": rep.params,
+        "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3)}
+    for precision in ("fp64", "fp32"):
+        surf5, _, sch5, plan5 = c5_setup(chains=125_000)
+        plan5.precision = precision
+        rep, secs = timed(lambda: eng.calibrate_case2_T2(surf5, None, sch5, plan5, None))
+        t = eng.last_timing()
+        out["c5_per_gpu_step" + ("" if precision == "fp64" else "_fp32")] = {
+            "metric": f"MC SABR path-steps/s, C5 per-GPU SA step (125,000 chains, default Case II box, {precision})",
+            "unit": "path-steps/s", "value": t.path_steps / secs, "seconds": secs, "cost_evals": rep.evals - 1,
+            "path_steps": t.path_steps, "kernel_path_steps_per_s": t.path_steps / (t.kernel_ms / 1e3),
+            "note": "proposals outside the Case II feasibility grid are skipped without an eval "
+                    "(annealer.cpp:122), as in the reference"}
+    return out
+
+
 def cpu_baseline(fx):
     """The compiled reference (oracle/_ref) on the host cores: the headline
     C2 sample at all threads (the line's cpu_baseline), plus the BASELINE.md
@@ -722,6 +771,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-configs", action="store_true",
+                    help="also run C4 as a whole calibration and C5 at its per-GPU size (about 3 minutes)")
     args = ap.parse_args()
     what, detail = launch_plan(args.gpus, os.environ, sys.argv[1:])
     if what == "error":
