@@ -154,10 +154,17 @@ cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const
 cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
                               double* alpha0, double* beta, uint8_t* active, cudaStream_t s);
 // per (candidate, step) coefficients of build_grid (mc.cpp:69-82) on device
-cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
-                           int32_t cand_stride, const double* t_end, const double* dt,
+cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int32_t* n_live, int32_t c0,
+                           int32_t n_local, int32_t cand_stride, const double* t_end, const double* dt,
                            const double* sdt, int64_t total_steps, void* coef, int fp32,
                            cudaStream_t s);
+// the step's feasible candidates compacted (t2_compact_kernel), and their
+// costs / non-finite flags scattered back to their chains
+cudaError_t launch_t2_compact(const uint8_t* active, const double* alpha0, const double* beta, int32_t n,
+                              int32_t* idx, double* alpha0_c, double* beta_c, uint8_t* active_c,
+                              int32_t* n_live, cudaStream_t s);
+cudaError_t launch_t2_scatter(const int32_t* idx, const int32_t* n_live, int32_t n, const double* cost_c,
+                              const int* bad_c, double* cost, int* bad, cudaStream_t s);
 // Metropolis (annealer.cpp:123-134) with the MC costs of this step
 cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double* cost,
                              const int* bad, int* nonfinite, cudaStream_t s);

@@ -1396,21 +1396,27 @@ __global__ void __launch_bounds__(32 * kProposeChainsPerCta)
 
 // coef[i][c] (step-major, cand_stride columns); inactive and padding
 // candidates get zero coefficients (simulated harmlessly, never priced).
-__global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t* __restrict__ active,
+// idx: the compacted candidate list (t2_compact_kernel): candidate c of the
+// launch is chain idx[c] (-1: no candidate); n_live: the list's length - a
+// launch that starts past it writes nothing (its MC blocks all exit).
+__global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const int32_t* __restrict__ idx,
+                               const int32_t* __restrict__ n_live, const int32_t c0,
                                const int32_t n_local, const int32_t cand_stride,
                                const double* __restrict__ t_end, const double* __restrict__ dt,
                                const double* __restrict__ sdt, const int64_t total_steps,
                                double4* __restrict__ coef, float4* __restrict__ coef32) {
+    if (c0 >= *n_live) return;  // uniform
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<int64_t>(cand_stride) * total_steps) return;
     const int c = static_cast<int>(t % cand_stride);
     const int64_t i = t / cand_stride;
-    if (c >= n_local || !active[c]) {
+    const int32_t chain = c < n_local ? idx[c0 + c] : -1;
+    if (chain < 0) {
         if (coef32) coef32[t] = make_float4(0.f, 0.f, 0.f, 0.f);
         else coef[t] = make_double4(0.0, 0.0, 0.0, 0.0);
         return;
     }
-    const T2Chain& ch = chains[c];
+    const T2Chain& ch = chains[chain];
     double p[11];
     for (int k = 0; k < 10; ++k) p[k] = ch.y[k];
     const double tt = t_end[i];
@@ -1423,6 +1429,74 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const uint8_t
     if (coef32) coef32[t] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
                                         static_cast<float>(v.z), static_cast<float>(v.w));
     else coef[t] = v;
+}
+
+// The step's candidates compacted (feasible proposals first, in chain
+// order): the MC launches then fill every CB-candidate group of a thread with
+// live work instead of simulating the infeasible proposals' zero rows (C5 in
+// the default box: ~45% of proposals).  A candidate's price does not depend
+// on its position in the batch (kernels_mc.cu), so results are unchanged.
+// One CTA: each thread scans a contiguous segment, then a CTA-wide scan of
+// the segment counts.
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads)
+    t2_compact_kernel(const uint8_t* __restrict__ active, const double* __restrict__ alpha0,
+                      const double* __restrict__ beta, const int32_t n, int32_t* __restrict__ idx,
+                      double* __restrict__ alpha0_c, double* __restrict__ beta_c, uint8_t* __restrict__ active_c,
+                      int32_t* __restrict__ n_live) {
+    __shared__ int32_t warp_tot[kCompactThreads / 32];
+    const int seg = (n + kCompactThreads - 1) / kCompactThreads;
+    const int b = threadIdx.x * seg, e = min(n, b + seg);
+    int cnt = 0;
+    for (int c = b; c < e; ++c) cnt += active[c] != 0;
+    // exclusive scan over the CTA: warp shuffles, then the warp totals
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = warp_tot[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += v;
+        }
+        warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    int k = incl - cnt + (warp > 0 ? warp_tot[warp - 1] : 0);
+    for (int c = b; c < e; ++c) {
+        if (active[c] == 0) continue;
+        idx[k] = c;
+        alpha0_c[k] = alpha0[c];
+        beta_c[k] = beta[c];
+        active_c[k] = 1;
+        ++k;
+    }
+    const int total = warp_tot[kCompactThreads / 32 - 1];
+    for (int c = total + threadIdx.x; c < n; c += kCompactThreads) {
+        idx[c] = -1;
+        alpha0_c[c] = 1.0;
+        beta_c[c] = 1.0;
+        active_c[c] = 0;
+    }
+    if (threadIdx.x == 0) *n_live = total;
+}
+
+// The compacted candidates' costs and non-finite flags back to their chains.
+__global__ void t2_scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_live,
+                                  const double* __restrict__ cost_c, const int* __restrict__ bad_c,
+                                  double* __restrict__ cost, int* __restrict__ bad) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *n_live) return;
+    const int c = idx[k];
+    cost[c] = cost_c[k];
+    bad[c] |= bad_c[k];
 }
 
 __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
@@ -1780,15 +1854,31 @@ cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2
     return cudaGetLastError();
 }
 
-cudaError_t launch_t2_coef(const T2Chain* chains, const uint8_t* active, int32_t n_local,
-                           int32_t cand_stride, const double* t_end, const double* dt,
+cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int32_t* n_live, int32_t c0,
+                           int32_t n_local, int32_t cand_stride, const double* t_end, const double* dt,
                            const double* sdt, int64_t total_steps, void* coef, int fp32,
                            cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(cand_stride) * total_steps;
     if (n <= 0) return cudaSuccess;
     t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        chains, active, n_local, cand_stride, t_end, dt, sdt, total_steps,
+        chains, idx, n_live, c0, n_local, cand_stride, t_end, dt, sdt, total_steps,
         fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_compact(const uint8_t* active, const double* alpha0, const double* beta, int32_t n,
+                              int32_t* idx, double* alpha0_c, double* beta_c, uint8_t* active_c,
+                              int32_t* n_live, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    t2_compact_kernel<<<1, kCompactThreads, 0, s>>>(active, alpha0, beta, n, idx, alpha0_c, beta_c, active_c,
+                                                    n_live);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_scatter(const int32_t* idx, const int32_t* n_live, int32_t n, const double* cost_c,
+                              const int* bad_c, double* cost, int* bad, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    t2_scatter_kernel<<<(n + 255) / 256, 256, 0, s>>>(idx, n_live, cost_c, bad_c, cost, bad);
     return cudaGetLastError();
 }
 

@@ -145,6 +145,14 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     auto* active = static_cast<uint8_t*>(dev_buf(ctx, "t2_active", nl));
     auto* cost = static_cast<double*>(dev_buf(ctx, "t2_cost", sizeof(double) * nl));
     auto* bad = static_cast<int*>(dev_buf(ctx, "t2_bad", sizeof(int) * nl));
+    // the step's feasible candidates, compacted (t2_compact_kernel)
+    auto* cidx = static_cast<int32_t*>(dev_buf(ctx, "t2_cidx", sizeof(int32_t) * nl));
+    auto* n_live = static_cast<int32_t*>(dev_buf(ctx, "t2_n_live", sizeof(int32_t)));
+    auto* alpha0_c = static_cast<double*>(dev_buf(ctx, "t2_alpha0_c", sizeof(double) * nl));
+    auto* beta_c = static_cast<double*>(dev_buf(ctx, "t2_beta_c", sizeof(double) * nl));
+    auto* active_c = static_cast<uint8_t*>(dev_buf(ctx, "t2_active_c", nl));
+    auto* cost_c = static_cast<double*>(dev_buf(ctx, "t2_cost_c", sizeof(double) * nl));
+    auto* bad_c = static_cast<int*>(dev_buf(ctx, "t2_bad_c", sizeof(int) * nl));
     auto* nonfinite = static_cast<int*>(dev_buf(ctx, "t2_nonfinite", sizeof(int)));
     void* coef = dev_buf(ctx, "t2_coef", (fp32 ? sizeof(float4) : sizeof(StepCoef)) * S * stride);
     auto* partials = static_cast<double*>(
@@ -204,23 +212,28 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
         for (int step = 0; step < sch.chain_length; ++step) {
             NvtxRange nvtx_step("sabr.t2_step");
             check_cuda(launch_t2_propose(chains, a.state, ta, alpha0, beta, active, ctx->stream), "t2_propose");
+            // the MC launches run over the compacted feasible candidates: a
+            // chunk past the live count exits in every kernel
+            check_cuda(launch_t2_compact(active, alpha0, beta, n_local, cidx, alpha0_c, beta_c, active_c, n_live,
+                                         ctx->stream), "t2_compact");
+            check_cuda(cudaMemsetAsync(bad_c, 0, sizeof(int) * nl, ctx->stream), "memset");
             for (int32_t c0 = 0; c0 < n_local; c0 += chunk) {
                 const int32_t nc = std::min(chunk, n_local - c0);
                 const int32_t nc_pad = (nc + cb - 1) / cb * cb;
-                check_cuda(launch_t2_coef(chains + c0, active + c0, nc, nc_pad, d_tend, d_dt, d_sdt, S,
+                check_cuda(launch_t2_coef(chains, cidx, n_live, c0, nc, nc_pad, d_tend, d_dt, d_sdt, S,
                                           coef, fp32 ? 1 : 0, ctx->stream), "t2_coef");
                 McParams Q = P;
                 Q.n_cand = nc;
-                Q.alpha0 = alpha0 + c0;
-                Q.beta = beta + c0;
-                Q.active = active + c0;
+                Q.alpha0 = alpha0_c + c0;
+                Q.beta = beta_c + c0;
+                Q.active = active_c + c0;
                 Q.fp32 = fp32 ? 1 : 0;
                 Q.coef = fp32 ? nullptr : static_cast<const StepCoef*>(coef);
                 Q.coef32 = fp32 ? static_cast<const float4*>(coef) : nullptr;
                 Q.cand_stride = nc_pad;
                 Q.partials = partials;
                 Q.terminals = nullptr;
-                Q.bad = bad + c0;
+                Q.bad = bad_c + c0;
                 Q.tile_begin = tile_begin;
                 Q.tile_count = tile_count;
                 timer.before();
@@ -230,10 +243,12 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
                     const size_t slab = sizeof(double) * 2 * static_cast<size_t>(tpr) * nc * nq;
                     allgather(ctx, reinterpret_cast<unsigned char*>(partials) + ctx->rank * slab, partials, slab);
                 }
-                check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, cost + c0, ctx->stream), "mc_reduce");
+                check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, cost_c + c0, ctx->stream), "mc_reduce");
                 mc_launches += 1;
                 launches += 4;
             }
+            check_cuda(launch_t2_scatter(cidx, n_live, n_local, cost_c, bad_c, cost, bad, ctx->stream), "t2_scatter");
+            launches += 2;
             check_cuda(launch_t2_accept(chains, ta, cost, bad, nonfinite, ctx->stream), "t2_accept");
             launches += 2;
         }
