@@ -199,6 +199,14 @@ SABR_D void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, ui
     out[3] = c3;
 }
 
+// the pair's two raw 64-bit draws (philox_uniform_pair = their top53 * 2^-64)
+SABR_D void philox_bits_pair(uint64_t seed, uint64_t path, uint32_t step, uint64_t& a, uint64_t& b) {
+    uint32_t x[4];
+    philox4x32_10(static_cast<uint32_t>(path), static_cast<uint32_t>(path >> 32), step, 0u, seed, x);
+    a = (static_cast<uint64_t>(x[0]) << 32) | x[1];
+    b = (static_cast<uint64_t>(x[2]) << 32) | x[3];
+}
+
 SABR_D void philox_uniform_pair(uint64_t seed, uint64_t path, uint32_t step, double& ua,
                                 double& ub) {
     uint32_t x[4];
@@ -428,6 +436,33 @@ SABR_D void box_muller_tab(double ua, double ub, const double4* __restrict__ log
     sincos_2pi(ub, sctab, s, c);
     z1 = r * c;
     z2 = r * s;
+}
+
+// Box-Muller for the FP32 MC path (mc.cpp:30-36) on two raw draws, on the
+// MUFU only: u1 = 1 - U1 from the integer (~m1 = 2^64 - 1 - m1 with m1 the
+// draw's 53 significant bits: in float this is 2^64 - m1 rounded, never 0,
+// and exactly 2^64 -> u1 = 1 for U1 = 0), r = sqrt(-2 ln2 lg2 u1), theta =
+// 2 pi U2 taken to [-pi, pi) for sin/cos.approx.  Absolute errors ~1e-6 in
+// the normals (lg2/sin/cos.approx ~2^-21), far inside the FP32 path's 2e-5
+// price tolerance; one LG2, one SQRT, one SIN, one COS and two I2F instead of
+// libm's logf/sqrtf/sincospif (~150 instructions per path-step with their
+// range reductions and slow-path calls).
+SABR_D void box_muller_f32_bits(uint64_t n1, uint64_t n2, float& z1, float& z2) {
+    const uint64_t m1 = n1 & ~0x7ffull, m2 = n2 & ~0x7ffull;
+    float lg, r, sn, cs;
+    // lg2 of u1 itself (in [2^-53, 1]), not of the 2^64-scaled integer: the
+    // result is near 0 when u1 is near 1 (small r), where float resolves it
+    // finely; near 64 its ulp (2^-17) made -2 ln u1 coarse by 1e-5 (measured:
+    // 8e-5 worst per-path error, 1.7e-6 with this form)
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(__ull2float_rn(~m1) * 0x1.0p-64f));
+    const float w = -1.38629436f * lg;  // -2 ln u1 >= 0
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(w));
+    const float u2 = __ull2float_rn(m2) * 0x1.0p-64f;
+    const float t = (u2 >= 0.5f ? u2 - 1.0f : u2) * 6.28318531f;  // 2 pi U2 in [-pi, pi)
+    asm("sin.approx.ftz.f32 %0, %1;" : "=f"(sn) : "f"(t));
+    asm("cos.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(t));
+    z1 = r * cs;
+    z2 = r * sn;
 }
 
 // ------------------------------------------------------------ analytics ---

@@ -296,19 +296,14 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
         }
         if (live) {
             auto normals = [&](int i, float& z1, float& z2) {
-                double ua, ub;
+                uint64_t na, nb;  // the step's two draws, in the reference's order
                 if (P.rng == SABR_RNG_XOSHIRO) {
-                    ua = rng.uniform();
-                    ub = rng.uniform();
+                    na = rng.next();
+                    nb = rng.next();
                 } else {
-                    philox_uniform_pair(P.seed, path, static_cast<uint32_t>(i), ua, ub);
+                    philox_bits_pair(P.seed, path, static_cast<uint32_t>(i), na, nb);
                 }
-                // box_muller, mc.cpp:30-36: u1 = 1 - U in (0,1] (exact in FP64)
-                const float r = sqrtf(-2.0f * logf(static_cast<float>(1.0 - ua)));
-                float sn, cs;
-                sincospif(static_cast<float>(2.0 * ub), &sn, &cs);
-                z1 = r * cs;
-                z2 = r * sn;
+                box_muller_f32_bits(na, nb, z1, z2);  // box_muller, mc.cpp:30-36
             };
             auto advance_all = [&](float h, const float4* q, float z1, float z2) {
 #pragma unroll
