@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
     //   x     += nu_hat (rho z1 + srho z2) sqrt(dt) - nu_hat^2 dt / 2  (mc.cpp:101-102)
     // Inactive / padding candidates have zero coefficients and are skipped in
     // the payoffs: no per-candidate branch in the step loop.
-    uint32_t act_mask = 0, logn_mask = 0;
+    uint32_t act_mask = 0;
     double la0[CB], bm1[CB];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) {
@@ -79,7 +79,6 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
         act_mask |= act ? (1u << cc) : 0u;
         la0[cc] = act ? log(P.alpha0[c]) : 0.0;
         bm1[cc] = act ? P.beta[c] - 1.0 : 0.0;
-        logn_mask |= (bm1[cc] == 0.0) ? (1u << cc) : 0u;  // beta == 1: nu_hat = alpha exactly
     }
     if (act_mask == 0) return;  // block-uniform
     __syncthreads();            // exp table staged
@@ -141,7 +140,9 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
             auto advance_all = [&](double h, double z1, double z2, const StepCoef* next) {
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
-                    const double arg = ((logn_mask >> cc) & 1u) ? la[cc] : fma(bm1[cc], lnf0 + x[cc], la[cc]);
+                    // beta == 1 (mc.cpp:99-100: nu_hat = alpha): bm1 = 0 exactly,
+                    // so the fma returns la exactly for any finite x - no select
+                    const double arg = fma(bm1[cc], lnf0 + x[cc], la[cc]);
                     const double nh = exp_tab<kExpRep>(arg, tab_lane);
                     la[cc] += fma(qa[cc].x, z1, -qa[cc].y);
                     const double u = fma(qb[cc].y, z2, qb[cc].x * z1);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
     const int mq = sl.q_end - sl.q_begin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    uint32_t act_mask = 0, logn_mask = 0;
+    uint32_t act_mask = 0;
     float la0[CB], bm1[CB];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) {
@@ -258,7 +259,6 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
         act_mask |= act ? (1u << cc) : 0u;
         la0[cc] = act ? static_cast<float>(log(P.alpha0[c])) : 0.0f;
         bm1[cc] = act ? static_cast<float>(P.beta[c] - 1.0) : 0.0f;
-        logn_mask |= (act && P.beta[c] == 1.0) || !act ? (1u << cc) : 0u;
     }
     if (act_mask == 0) return;  // block-uniform
 
@@ -308,8 +308,9 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
             auto advance_all = [&](float h, const float4* q, float z1, float z2) {
 #pragma unroll
                 for (int cc = 0; cc < CB; ++cc) {
-                    const float arg = ((logn_mask >> cc) & 1u) ? la[cc] : fmaf(bm1[cc], lnf0 + x[cc], la[cc]);
-                    const float nh = __expf(arg);  // MUFU.EX2
+                    const float arg = fmaf(bm1[cc], lnf0 + x[cc], la[cc]);  // bm1 = 0 for beta == 1
+                    float nh;  // exp(arg) as one FMUL + MUFU.EX2 (flush-to-zero: no denormal rescaling)
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh) : "f"(arg * 1.44269504f));
                     la[cc] += fmaf(q[cc].x, z1, -q[cc].y);
                     const float u = fmaf(q[cc].w, z2, q[cc].z * z1);
                     x[cc] = fmaf(nh, fmaf(-nh, h, u), x[cc]);
