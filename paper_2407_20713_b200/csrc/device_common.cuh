@@ -107,6 +107,10 @@ struct Xoshiro {
     static SABR_HD double top53(uint64_t n) { return static_cast<double>(n & ~0x7ffull); }
     // the uniform() that the next draw would return, without drawing it
     SABR_HD double peek_uniform() const { return top53(rotl64c<23>(s0 + s3) + s0) * 0x1.0p-64; }
+    // the output next() would return (the raw 64-bit draw), without drawing it
+    SABR_HD uint64_t peek() const { return rotl64c<23>(s0 + s3) + s0; }
+    // 2 * uniform() - 1 of a raw draw n (sym() without the draw)
+    static SABR_HD double sym_of(uint64_t n) { return fma(top53(n), 0x1.0p-63, -1.0); }
     // the next draw's 53 significant bits in place: uniform() = peek_bits() * 2^-64 exactly
     SABR_HD uint64_t peek_bits() const { return (rotl64c<23>(s0 + s3) + s0) & ~0x7ffull; }
     // advance() when p, in place and without selects: the eight 32-bit words

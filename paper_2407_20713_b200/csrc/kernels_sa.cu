@@ -953,7 +953,13 @@ constexpr int rep_copies() { return KIND == OBJ_STATIC ? kExpRep : 4; }
 // level-end arg-min (annealer.cpp:141-159): on return (all threads) rs holds
 // the CTA's (endpoint, best) winners and eval count, rec their points.
 // Shared by the per-level kernel and the single-CTA persistent kernel.
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT>
+// PIPE (ALLFREE only): the RNG is software-pipelined - the draws of step s + 1
+// are generated while step s's objective runs, for both Metropolis outcomes,
+// and selected once fy is known.  That takes the xoshiro chain off the
+// critical path at the price of ~8 instructions per chain-step: a gain for
+// the latency-bound one-CTA run (C1: one warp per SM), a loss for the
+// issue-bound full-GPU level kernel (C2: -3.6%).
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT, bool PIPE = false>
 __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const ObjGrid<GK>& g,
                                                  const double2* tab_s, const double2* tab_lane,
                                                  const double* pw_fixed,
@@ -986,12 +992,32 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             if constexpr (GK == kGridQR) sl = qr_slice(g);
             else sl = static_slice(g);
         }
+        // PIPE: ws holds this step's proposal draws as 2u - 1, cand the
+        // Metropolis candidate o_{p+D} and rng the state that produces it;
+        // step s computes o_{p+D+1} .. o_{p+2D} (rng ends at S_{p+2D}), and
+        // once fy is known, step s + 1 takes o_{p+D+1 ..} when the candidate
+        // was consumed (fy > fx) and o_{p+D ..} otherwise.
+        constexpr bool kPipe = PIPE && ALLFREE;
+        double ws[C][kPipe ? DIMF : 1];
+        uint64_t cand[C];
+        if constexpr (kPipe) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+#pragma unroll
+                for (int i = 0; i < DIMF; ++i) ws[c][i] = rng[c].sym();
+                cand[c] = rng[c].peek();
+            }
+        }
         for (int step = 0; step < steps; ++step) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
 #pragma unroll
                 for (int i = 0; i < DIMF; ++i) {
-                    if (ALLFREE)
+                    if (kPipe) {
+                        const double v = __dadd_rn(x[c][i], __dmul_rn(step_scale[i], ws[c][i]));
+                        const double rh = __dsub_rn(a.hi2[i], v), rl = __dsub_rn(a.lo2[i], v);
+                        y[c][i] = (v > a.hi[i]) ? rh : (v < a.lo[i]) ? rl : v;
+                    } else if (ALLFREE)
                         y[c][i] = propose_coord_fast(x[c][i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i],
                                                      a.hi2[i], rng[c]);
                     else if ((a.free_mask >> i) & 1u)
@@ -1006,10 +1032,18 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             // before the objective is (metropolis_fast)
             uint64_t mbits[C];
             float tau[C];
+            double nsym[C][kPipe ? DIMF + 1 : 1];  // PIPE: 2u - 1 of o_{p+D} .. o_{p+2D}
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                mbits[c] = rng[c].peek_bits();
+                mbits[c] = kPipe ? cand[c] & ~0x7ffull : rng[c].peek_bits();
                 tau[c] = neg_log_uniform(mbits[c]);
+                if constexpr (kPipe) {
+                    nsym[c][0] = Xoshiro::sym_of(cand[c]);
+                    rng[c].advance();  // past the candidate
+#pragma unroll
+                    for (int j = 1; j <= DIMF; ++j)
+                        nsym[c][j] = Xoshiro::sym_of(j < DIMF ? rng[c].next() : rng[c].peek());
+                }
             }
             double fy[C];
             if constexpr (KIND == OBJ_STATIC) {
@@ -1032,7 +1066,15 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             for (int c = 0; c < C; ++c) {
                 if (isnan(fy[c])) fy[c] = CUDART_INF;
                 unsure |= metropolis_fast(fy[c], fx[c], inv_temp, tau[c]).unsure;
-                rng[c].advance_if(!(fy[c] <= fx[c]));
+                const bool up = !(fy[c] <= fx[c]);
+                if constexpr (kPipe) {
+#pragma unroll
+                    for (int i = 0; i < DIMF; ++i) ws[c][i] = up ? nsym[c][i + 1] : nsym[c][i];
+                    rng[c].advance_if(up);  // S_{p+2D} -> S_{p+2D+1} when the draw was consumed
+                    cand[c] = rng[c].peek();
+                } else {
+                    rng[c].advance_if(up);
+                }
             }
             if (unsure) {
 #pragma unroll
@@ -1195,8 +1237,8 @@ __global__ void __launch_bounds__(kLevelThreads / C, 1)
 #pragma unroll
         for (int c = 0; c < C; ++c)
             rng[c].init(a.seed, (static_cast<uint64_t>(level) << 20) ^ static_cast<uint64_t>(chain[c]));
-        run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, nullptr, pw_fixed, st, temp, inv_temp,
-                                                         active, chain, rng, bp_s, rs, rec);
+        run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT, true>(a, g, tab_s, nullptr, pw_fixed, st, temp,
+                                                               inv_temp, active, chain, rng, bp_s, rs, rec);
         if (threadIdx.x == 0) {
             sabr_level_record out;
             const bool e_ok = rs.e_win.i != LLONG_MAX, b_ok = rs.b_win.i != LLONG_MAX;
