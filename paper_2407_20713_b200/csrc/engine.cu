@@ -180,14 +180,18 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 // 2lo - v <= hi hold at those extremes, the reference's second reflection and
 // its clamp never change the value, and the level kernels use
 // propose_coord_fast (same bits, fewer compares).
-bool single_reflection(const SaLevelArgs& a, int dim_full) {
+// free_only: the property for the searched dims (fixed dims never move)
+bool single_reflection(const SaLevelArgs& a, int dim_full, bool free_only = false) {
     static const bool enabled = [] {  // SABR_SA_FAST=0: general propose (A/B checks)
         const char* e = std::getenv("SABR_SA_FAST");
         return !(e && std::atoi(e) == 0);
     }();
     if (!enabled) return false;
     for (int i = 0; i < dim_full; ++i) {
-        if (!((a.free_mask >> i) & 1u)) return false;
+        if (!((a.free_mask >> i) & 1u)) {
+            if (free_only) continue;
+            return false;
+        }
         const double vmax = a.hi[i] + a.range[i] * (1.0 - 0x1.0p-52), vmin = a.lo[i] - a.range[i];
         if (!std::isfinite(vmax) || !std::isfinite(vmin) || !std::isfinite(a.hi2[i]) ||
             !std::isfinite(a.lo2[i]))
@@ -256,6 +260,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     }
     a.free_mask = free_mask;
     a.fast = single_reflection(a, dim_full) ? 1 : 0;
+    a.fast_free = single_reflection(a, dim_full, true) ? 1 : 0;
     a.dim_full = dim_full;
     a.chain_length = sch.chain_length;
     a.builtin = builtin;

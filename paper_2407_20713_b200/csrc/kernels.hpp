@@ -77,6 +77,7 @@ struct SaLevelArgs {
     int32_t predicate;           // SABR_PRED_*
     int32_t nranks;
     int32_t fast;                // all dims free and one reflection always lands in the box
+    int32_t fast_free;           // one reflection always lands in the box for every searched dim
     double t0;
     uint64_t seed;
     int64_t chain_begin;         // global index of this rank's first chain

@@ -959,7 +959,10 @@ constexpr int rep_copies() { return KIND == OBJ_STATIC ? kExpRep : 4; }
 // critical path at the price of ~8 instructions per chain-step: a gain for
 // the latency-bound one-CTA run (C1: one warp per SM), a loss for the
 // issue-bound full-GPU level kernel (C2: -3.6%).
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT, bool PIPE = false>
+// FIXM (with ALLFREE false): a compile-time mask of fixed coordinates, every
+// other coordinate searched with the one-reflection propose (a.fast_free);
+// Case I with beta fixed, the C3 configuration, uses FIXM = 2.
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT, bool PIPE = false, int FIXM = 0>
 __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const ObjGrid<GK>& g,
                                                  const double2* tab_s, const double2* tab_lane,
                                                  const double* pw_fixed,
@@ -997,14 +1000,19 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
         // step s computes o_{p+D+1} .. o_{p+2D} (rng ends at S_{p+2D}), and
         // once fy is known, step s + 1 takes o_{p+D+1 ..} when the candidate
         // was consumed (fy > fx) and o_{p+D ..} otherwise.
-        constexpr bool kPipe = PIPE && ALLFREE;
+        constexpr uint32_t kFull = (1u << DIMF) - 1u;
+        constexpr bool kFastProp = ALLFREE || FIXM != 0;
+        constexpr uint32_t kFree = ALLFREE ? kFull : (kFull & ~static_cast<uint32_t>(FIXM));
+        constexpr int kDraws = __builtin_popcount(kFree);  // draws per step on the fast path
+        constexpr bool kPipe = PIPE && kFastProp;
         double ws[C][kPipe ? DIMF : 1];
         uint64_t cand[C];
         if constexpr (kPipe) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
 #pragma unroll
-                for (int i = 0; i < DIMF; ++i) ws[c][i] = rng[c].sym();
+                for (int i = 0; i < DIMF; ++i)
+                    if ((kFree >> i) & 1u) ws[c][i] = rng[c].sym();
                 cand[c] = rng[c].peek();
             }
         }
@@ -1013,11 +1021,13 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             for (int c = 0; c < C; ++c) {
 #pragma unroll
                 for (int i = 0; i < DIMF; ++i) {
-                    if (kPipe) {
+                    if (kFastProp && !((kFree >> i) & 1u)) {
+                        y[c][i] = x[c][i];  // fixed coordinate (FIXM)
+                    } else if (kPipe) {
                         const double v = __dadd_rn(x[c][i], __dmul_rn(step_scale[i], ws[c][i]));
                         const double rh = __dsub_rn(a.hi2[i], v), rl = __dsub_rn(a.lo2[i], v);
                         y[c][i] = (v > a.hi[i]) ? rh : (v < a.lo[i]) ? rl : v;
-                    } else if (ALLFREE)
+                    } else if (kFastProp)
                         y[c][i] = propose_coord_fast(x[c][i], step_scale[i], a.lo[i], a.hi[i], a.lo2[i],
                                                      a.hi2[i], rng[c]);
                     else if ((a.free_mask >> i) & 1u)
@@ -1032,7 +1042,7 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
             // before the objective is (metropolis_fast)
             uint64_t mbits[C];
             float tau[C];
-            double nsym[C][kPipe ? DIMF + 1 : 1];  // PIPE: 2u - 1 of o_{p+D} .. o_{p+2D}
+            double nsym[C][kPipe ? kDraws + 1 : 1];  // PIPE: 2u - 1 of o_{p+D} .. o_{p+2D}
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 mbits[c] = kPipe ? cand[c] & ~0x7ffull : rng[c].peek_bits();
@@ -1041,8 +1051,8 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
                     nsym[c][0] = Xoshiro::sym_of(cand[c]);
                     rng[c].advance();  // past the candidate
 #pragma unroll
-                    for (int j = 1; j <= DIMF; ++j)
-                        nsym[c][j] = Xoshiro::sym_of(j < DIMF ? rng[c].next() : rng[c].peek());
+                    for (int j = 1; j <= kDraws; ++j)
+                        nsym[c][j] = Xoshiro::sym_of(j < kDraws ? rng[c].next() : rng[c].peek());
                 }
             }
             double fy[C];
@@ -1069,7 +1079,11 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
                 const bool up = !(fy[c] <= fx[c]);
                 if constexpr (kPipe) {
 #pragma unroll
-                    for (int i = 0; i < DIMF; ++i) ws[c][i] = up ? nsym[c][i + 1] : nsym[c][i];
+                    for (int i = 0; i < DIMF; ++i) {
+                        if (!((kFree >> i) & 1u)) continue;
+                        const int r = __popc(kFree & ((1u << i) - 1u));  // the draw's slot (constant)
+                        ws[c][i] = up ? nsym[c][r + 1] : nsym[c][r];
+                    }
                     rng[c].advance_if(up);  // S_{p+2D} -> S_{p+2D+1} when the draw was consumed
                     cand[c] = rng[c].peek();
                 } else {
@@ -1124,7 +1138,7 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
     __syncthreads();
 }
 
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C>
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int FIXM = 0, bool PIPE = false>
 __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
@@ -1182,8 +1196,8 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
             pw_fixed = pw_s;
         }
     }
-    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT>(a, g, tab_s, tab_lane, pw_fixed, st, temp, inv_temp, active,
-                                                     chain, rng, bp_s, rs, rec);
+    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT, PIPE, FIXM>(a, g, tab_s, tab_lane, pw_fixed, st, temp,
+                                                                 inv_temp, active, chain, rng, bp_s, rs, rec);
     if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
     reduce_block_records<NT, DIMF>(rs, a, level);
 }
@@ -1671,6 +1685,14 @@ bool pdl_enabled() {
     return on;
 }
 
+bool pipe_enabled() {  // SABR_SA_PIPE=1: software-pipelined RNG in the C3 level kernel (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("SABR_SA_PIPE");
+        return e && std::atoi(e) == 1;
+    }();
+    return on;
+}
+
 template <int KIND, int DIMF>
 cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, double temp,
                     cudaStream_t s) {
@@ -1702,7 +1724,16 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
                               sa_level_multi_kernel<KIND, DIMF, true, kGridQuads, 2>};
             const K kq3[2] = {sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 3>,
                               sa_level_multi_kernel<KIND, DIMF, true, kGridQR, 3>};
-            const K k = (gk == kGridQR ? (cpt == 1 ? kq1 : cpt == 3 ? kq3 : kq2) : kp2)[all_free ? 1 : 0];
+            K k = (gk == kGridQR ? (cpt == 1 ? kq1 : cpt == 3 ? kq3 : kq2) : kp2)[all_free ? 1 : 0];
+            // Case I with beta fixed (C3): the one-reflection propose on the
+            // searched dims, beta held (FIXM = bit 1); SABR_SA_PIPE=1 adds the
+            // software-pipelined RNG (A/B)
+            if constexpr (KIND == OBJ_CASE1 && DIMF == 6) {
+                if (gk == kGridQR && cpt == 2 && !all_free && a.fast_free != 0 &&
+                    a.free_mask == ((1u << DIMF) - 1u & ~2u))
+                    k = pipe_enabled() ? sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, true>
+                                       : sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, false>;
+            }
             const int ntc = gk == kGridQR && cpt == 3 ? 3 : (gk == kGridQR && cpt == 1 ? 1 : 2);
             const unsigned threads = static_cast<unsigned>(ntc == 3 ? level_nt<3>() : ntc == 1 ? level_nt<1>() : level_nt<2>());
             const unsigned grid = static_cast<unsigned>((a.n_local + threads * ntc - 1) / (threads * ntc));
