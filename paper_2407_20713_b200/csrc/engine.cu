@@ -677,11 +677,12 @@ void set_coefficients(sabr_ctx* ctx, McParams& P, const std::vector<StepCoef>& c
     P.coef = upload(ctx, "mc_coef", coef);
     P.fp32 = precision == SABR_FP32 ? 1 : 0;
     P.coef32 = nullptr;
-    if (P.fp32) {
+    if (P.fp32) {  // {c1, -c2, rs, ss} * log2(e): mc_tile_kernel_f32's base-2 state (one candidate)
+        constexpr double kLog2e = 1.4426950408889634;
         std::vector<float4> c32(coef.size());
         for (size_t i = 0; i < coef.size(); ++i)
-            c32[i] = make_float4(static_cast<float>(coef[i].c1), static_cast<float>(coef[i].c2),
-                                 static_cast<float>(coef[i].rs), static_cast<float>(coef[i].ss));
+            c32[i] = make_float4(static_cast<float>(coef[i].c1 * kLog2e), static_cast<float>(-coef[i].c2 * kLog2e),
+                                 static_cast<float>(coef[i].rs * kLog2e), static_cast<float>(coef[i].ss * kLog2e));
         P.coef32 = upload(ctx, "mc_coef32", c32);
     }
 }

@@ -157,7 +157,7 @@ cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2
 // per (candidate, step) coefficients of build_grid (mc.cpp:69-82) on device
 cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int32_t* n_live, int32_t c0,
                            int32_t n_local, int32_t cand_stride, const double* t_end, const double* dt,
-                           const double* sdt, int64_t total_steps, void* coef, int fp32,
+                           const double* sdt, int64_t total_steps, void* coef, int fp32 /* 0 FP64, 1 FP32, 2 FP32 pair-interleaved */,
                            cudaStream_t s);
 // the step's feasible candidates compacted (t2_compact_kernel), and their
 // costs / non-finite flags scattered back to their chains

@@ -228,13 +228,90 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
     }
 }
 
-// The FP32 fast path: the same streams (uniforms drawn in FP64 exactly as the
-// reference draws them), the same log-Euler step carried in FP32 state with
-// one MUFU ex2 per candidate-step; normals from accurate FP32 library
-// functions; F_T = F0 exp(x) and the payoff sums in FP64.
+// Per-warp payoff sums by a shared-memory transpose (FP32 kernel, r02): each
+// lane writes its discounted payoffs and their squares for 16 (candidate,
+// quote, moment) columns as one row of a [32][17] tile; then the two
+// half-warps each sum 16 rows of one column and meet with one shuffle.  Per
+// value that is one STS, one LDS and one DADD, where two 5-level warp_sum
+// trees cost ten shuffles and five DADD; the order (lanes 0-15 and 16-31 in
+// four interleaved partial sums each, then the halves) is fixed, so a price
+// still depends only on (num_paths, ppt).
+constexpr int kTrCols = 16;
+constexpr int kTrStride = kTrCols + 1;  // 64-bit rows 17 doubles apart: no bank conflicts
+
+__device__ __forceinline__ void tr_flush(double* __restrict__ tb, double* __restrict__ accw, int base,
+                                         int ncols, int lane) {
+    __syncwarp();
+    const int col = lane & (kTrCols - 1), r0 = lane & kTrCols;  // rows 0-15 or 16-31
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < kTrCols; r += 4) {
+        s0 += tb[(r0 + r) * kTrStride + col];
+        s1 += tb[(r0 + r + 1) * kTrStride + col];
+        s2 += tb[(r0 + r + 2) * kTrStride + col];
+        s3 += tb[(r0 + r + 3) * kTrStride + col];
+    }
+    double s = (s0 + s1) + (s2 + s3);
+    const double o = __shfl_xor_sync(0xffffffffu, s, kTrCols);
+    s = (lane < kTrCols) ? s + o : o + s;  // the same sum on both halves
+    if (lane < ncols) accw[base + lane] += s;
+    __syncwarp();
+}
+
+// Discounted call payoffs of one path for every (candidate, quote), mc.cpp:265-269,
+// added to the warp's accumulators accw[(cc * mq + j) * 2 + {0, 1}].
+template <int CB>
+__device__ __forceinline__ void payoff_sums_tr(const double (&F)[CB], bool live, uint32_t act_mask,
+                                               const double* __restrict__ K, int mq, double disc,
+                                               double* __restrict__ tb, double* __restrict__ accw,
+                                               int lane) {
+    double* row = tb + lane * kTrStride;
+    int col = 0, base = 0;
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+        const bool on = live && ((act_mask >> cc) & 1u);
+        for (int j = 0; j < mq; ++j) {
+            const double d = F[cc] - __ldg(K + j);
+            const double v = on ? disc * ((d < 0.0) ? 0.0 : d) : 0.0;
+            row[col] = v;
+            row[col + 1] = v * v;
+            col += 2;
+            if (col == kTrCols) {
+                tr_flush(tb, accw, base, kTrCols, lane);
+                base += kTrCols;
+                col = 0;
+            }
+        }
+    }
+    if (col > 0) tr_flush(tb, accw, base, col, lane);
+}
+
+// The FP32 fast path (SABR_FP32): the same streams, the reference's log-Euler
+// step in FP32 state, one MUFU ex2 per candidate-step; F_T and the payoff
+// sums in FP64.  r02: the state is carried in base-2 logarithms,
+//   A = log2(alpha) + (beta - 1) log2(F0)   (so nu_hat = 2^(A + (beta-1) Y))
+//   Y = log2(F / F0),
+// with the coefficients pre-scaled by log2(e) (kernels_sa.cu t2_coef_kernel,
+// engine.cu set_coefficients), so a candidate-step is
+//   nu_hat = ex2(fma(beta - 1, Y, A));  A += c1 z1 - c2;
+//   Y += nu_hat (rs z1 + ss z2 - nu_hat h)
+// and two candidates share every instruction but the ex2 as packed FP32x2
+// (FFMA2 / FADD2 / FMUL2, the normals as broadcast operands): 4.5 instead of
+// 10 instructions per candidate-step.  CB >= 2 reads the pair-interleaved
+// coefficient rows (McParams::coef32_pairs): per pair and step
+// {c1 c1' -c2 -c2'} {rs rs' ss ss'}; CB = 1 reads {c1 -c2 rs ss}.
+// CTAs per SM of the FP32 kernel: its packed state fits 76 (time-invariant
+// rows) / 95 registers without spills in the step loop at CB <= 8, so 6 / 5
+// CTAs (24 / 20 warps per SM) hide the MUFU and FFMA2 latencies (r02: at 4
+// CTAs ncu showed 1.4 eligible warps per scheduler, "wait" the top stall)
 template <int CB, bool CONST>
-__global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid_constant__ McParams P) {
-    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
+constexpr int f32_min_ctas() { return CB <= 8 ? (CONST ? 6 : 5) : 4; }
+
+template <int CB, bool CONST>
+__global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
+    mc_tile_kernel_f32(const __grid_constant__ McParams P) {
+    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2], then [kWarps][32][kTrStride]
+    constexpr int NP = (CB + 1) / 2;                // candidate pairs (CB = 1: one, its odd half idle)
 
     int64_t idx = blockIdx.x;
     const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
@@ -251,18 +328,26 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     uint32_t act_mask = 0;
-    float la0[CB], bm1[CB];
+    float2 a0[NP], bm1[NP];
 #pragma unroll
-    for (int cc = 0; cc < CB; ++cc) {
+    for (int cc = 0; cc < 2 * NP; ++cc) {
         const int c = c0 + cc;
-        const bool act = c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
+        const bool act = cc < CB && c < P.n_cand && (P.active == nullptr || P.active[c] != 0);
         act_mask |= act ? (1u << cc) : 0u;
-        la0[cc] = act ? static_cast<float>(log(P.alpha0[c])) : 0.0f;
-        bm1[cc] = act ? static_cast<float>(P.beta[c] - 1.0) : 0.0f;
+        const double b1 = act ? P.beta[c] - 1.0 : 0.0;
+        const float a = act ? static_cast<float>((log(P.alpha0[c]) + b1 * sl.lnf0) * 1.4426950408889634) : 0.0f;
+        if (cc & 1) {
+            a0[cc >> 1].y = a;
+            bm1[cc >> 1].y = static_cast<float>(b1);
+        } else {
+            a0[cc >> 1].x = a;
+            bm1[cc >> 1].x = static_cast<float>(b1);
+        }
     }
     if (act_mask == 0) return;  // block-uniform
 
     const bool reduce = P.partials != nullptr;
+    double* tb = acc + kWarps * CB * mq * 2 + warp * 32 * kTrStride;
     if (reduce) {
         for (int i = threadIdx.x; i < kWarps * CB * mq * 2; i += kMcThreads) acc[i] = 0.0;
         __syncthreads();
@@ -280,19 +365,20 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
         rng.jump(pl);
     }
 
-    const int64_t cstride = P.cand_stride;
-    const float4* __restrict__ crow0 = P.coef32 + static_cast<int64_t>(sl.step_off) * cstride + c0;
+    // coefficient rows as float4: CB >= 2 two per pair (pair layout), CB = 1 one
+    constexpr int NQ = CB >= 2 ? 2 * NP : 1;
+    const int64_t rstride = P.cand_stride;  // float4s per step row (CB >= 2: cand_stride is even)
+    const float4* __restrict__ crow0 = P.coef32 + static_cast<int64_t>(sl.step_off) * rstride + c0;
     const double* __restrict__ hdt = P.hdt + sl.step_off;
-    const float lnf0 = static_cast<float>(sl.lnf0);
 
     for (int k = 0; k < P.ppt; ++k) {
         const uint64_t path = p0 + k;
         const bool live = path < P.num_paths;
-        float la[CB], x[CB];
+        float2 A[NP], Y[NP];
 #pragma unroll
-        for (int cc = 0; cc < CB; ++cc) {
-            la[cc] = la0[cc];
-            x[cc] = 0.0f;
+        for (int p = 0; p < NP; ++p) {
+            A[p] = a0[p];
+            Y[p] = make_float2(0.0f, 0.0f);
         }
         if (live) {
             auto normals = [&](int i, float& z1, float& z2) {
@@ -305,24 +391,42 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
                 }
                 box_muller_f32_bits(na, nb, z1, z2);  // box_muller, mc.cpp:30-36
             };
-            auto advance_all = [&](float h, const float4* q, float z1, float z2) {
+            // q[2p] = {c1, c1', -c2, -c2'}, q[2p+1] = {rs, rs', ss, ss'} (CB = 1: q[0] = {c1, -c2, rs, ss})
+            auto advance_all = [&](float nh_scale, const float4 (&q)[NQ], float z1, float z2) {
+                const float2 Z1 = make_float2(z1, z1), Z2 = make_float2(z2, z2);
+                const float2 H = make_float2(nh_scale, nh_scale);  // -h log2(e)
 #pragma unroll
-                for (int cc = 0; cc < CB; ++cc) {
-                    const float arg = fmaf(bm1[cc], lnf0 + x[cc], la[cc]);  // bm1 = 0 for beta == 1
-                    float nh;  // exp(arg) as one FMUL + MUFU.EX2 (flush-to-zero: no denormal rescaling)
-                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh) : "f"(arg * 1.44269504f));
-                    la[cc] += fmaf(q[cc].x, z1, -q[cc].y);
-                    const float u = fmaf(q[cc].w, z2, q[cc].z * z1);
-                    x[cc] = fmaf(nh, fmaf(-nh, h, u), x[cc]);
+                for (int p = 0; p < NP; ++p) {
+                    float2 c1, nc2, rs, ss;
+                    if constexpr (CB >= 2) {
+                        c1 = make_float2(q[2 * p].x, q[2 * p].y);
+                        nc2 = make_float2(q[2 * p].z, q[2 * p].w);
+                        rs = make_float2(q[2 * p + 1].x, q[2 * p + 1].y);
+                        ss = make_float2(q[2 * p + 1].z, q[2 * p + 1].w);
+                    } else {
+                        c1 = make_float2(q[0].x, 0.0f);
+                        nc2 = make_float2(q[0].y, 0.0f);
+                        rs = make_float2(q[0].z, 0.0f);
+                        ss = make_float2(q[0].w, 0.0f);
+                    }
+                    const float2 arg = __ffma2_rn(bm1[p], Y[p], A[p]);
+                    float2 nh;  // 2^arg, MUFU.EX2 (flush-to-zero: no denormal rescaling)
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh.x) : "f"(arg.x));
+                    if constexpr (CB >= 2) asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh.y) : "f"(arg.y));
+                    else nh.y = 0.0f;
+                    A[p] = __fadd2_rn(__ffma2_rn(c1, Z1, A[p]), nc2);
+                    const float2 u = __ffma2_rn(ss, Z2, __fmul2_rn(rs, Z1));
+                    Y[p] = __ffma2_rn(nh, __ffma2_rn(nh, H, u), Y[p]);
                 }
             };
-            // step i+1's coefficients are loaded while step i computes (the
-            // L1 latency of these uniform loads was the top stall)
-            float4 q[CB], qn[CB];
-            const float4* crow = crow0;
+            auto load = [&](float4 (&q)[NQ], const float4* row) {
 #pragma unroll
-            for (int cc = 0; cc < CB; ++cc) qn[cc] = __ldg(crow + cc);
-            float hn = static_cast<float>(__ldg(hdt));
+                for (int i = 0; i < NQ; ++i) q[i] = __ldg(row + i);
+            };
+            float4 q[NQ], qn[NQ];
+            const float4* crow = crow0;
+            load(qn, crow);
+            float hn = static_cast<float>(-__ldg(hdt) * 1.4426950408889634);
             float z1, z2;
             normals(0, z1, z2);
             const int n = sl.n_steps;
@@ -337,17 +441,16 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
                 }
                 advance_all(hn, qn, z1, z2);
             } else {
-            // unrolled by 2 so the q <- qn rotation is register renaming, not
-            // 4*CB moves per step (392 -> 341 instructions per step at CB = 8)
+            // unrolled by 2 so the q <- qn rotation is register renaming;
+            // step i+1's row is loaded while step i computes
 #pragma unroll 2
             for (int i = 0; i + 1 < n; ++i) {
 #pragma unroll
-                for (int cc = 0; cc < CB; ++cc) q[cc] = qn[cc];
+                for (int t = 0; t < NQ; ++t) q[t] = qn[t];
                 const float h = hn;
-                crow += cstride;
-#pragma unroll
-                for (int cc = 0; cc < CB; ++cc) qn[cc] = __ldg(crow + cc);
-                hn = static_cast<float>(__ldg(hdt + i + 1));
+                crow += rstride;
+                load(qn, crow);
+                hn = static_cast<float>(-__ldg(hdt + i + 1) * 1.4426950408889634);
                 float n1, n2;
                 normals(i + 1, n1, n2);
                 advance_all(h, q, z1, z2);
@@ -360,27 +463,14 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel_f32(const __grid
         double F[CB];
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc) {
-            F[cc] = sl.forward0 * exp(static_cast<double>(x[cc]));
+            const float y = (cc & 1) ? Y[cc >> 1].y : Y[cc >> 1].x;
+            F[cc] = sl.forward0 * exp2(static_cast<double>(y));
             if (live && ((act_mask >> cc) & 1u) && !isfinite(F[cc])) atomicOr(P.bad + c0 + cc, 1);
         }
         if (P.terminals != nullptr && live) P.terminals[path] = F[0];
         if (!reduce) continue;
-        for (int j = 0; j < mq; ++j) {
-            const double K = __ldg(P.strikes + sl.q_begin + j);
-#pragma unroll
-            for (int cc = 0; cc < CB; ++cc) {
-                if (!((act_mask >> cc) & 1u)) continue;
-                const double d = F[cc] - K;
-                const double v = live ? sl.discount * ((d < 0.0) ? 0.0 : d) : 0.0;
-                const double s1 = warp_sum(v);
-                const double s2 = warp_sum(v * v);
-                if (lane == 0) {
-                    double* slot = acc + ((warp * CB + cc) * mq + j) * 2;
-                    slot[0] += s1;
-                    slot[1] += s2;
-                }
-            }
-        }
+        payoff_sums_tr<CB>(F, live, act_mask, P.strikes + sl.q_begin, mq, sl.discount, tb,
+                           acc + warp * CB * mq * 2, lane);
     }
     if (!reduce) return;
     __syncthreads();
@@ -563,7 +653,10 @@ __global__ void mc_cost_kernel(const McParams P, const double* __restrict__ valu
 template <int CB>
 cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     const int mq = p.max_q;
-    const size_t smem = p.partials ? static_cast<size_t>(kWarps) * CB * mq * 2 * sizeof(double) : 0;
+    // FP32: the warps' payoff transpose tiles follow the accumulators (payoff_sums_tr)
+    const size_t smem = p.partials ? (static_cast<size_t>(kWarps) * CB * mq * 2 +
+                                      (p.fp32 ? static_cast<size_t>(kWarps) * 32 * kTrStride : 0)) * sizeof(double)
+                                   : 0;
     bool cst = p.n_slices > 0;
     for (int i = 0; i < p.n_slices; ++i) cst = cst && p.host_slices != nullptr && p.host_slices[i].const_coef;
     auto k = p.fp32 ? (cst ? mc_tile_kernel_f32<CB, true> : mc_tile_kernel_f32<CB, false>)

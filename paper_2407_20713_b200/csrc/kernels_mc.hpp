@@ -64,7 +64,8 @@ struct McParams {
     const double4* logtab;  // [128] log_tab entries (Box-Muller's log, device_common.cuh)
     const double2* sctab;   // [128] sincos_2pi entries (Box-Muller's angle)
     int32_t fp32;           // SABR_FP32: the FP32/MUFU path loop (coef32 instead of coef)
-    const float4* coef32;   // [total_steps][cand_stride] {c1, c2, rs, ss} in FP32
+    const float4* coef32;   // [total_steps][cand_stride] FP32 {c1, -c2, rs, ss} * log2(e); launches with
+                            // CB >= 2 read it pair-interleaved (kernels_sa.cu put_coef32)
 };
 
 // The exp_tab and log_tab tables, built once on the host in long double.

@@ -1452,6 +1452,28 @@ __global__ void __launch_bounds__(32 * kProposeChainsPerCta)
 
 // coef[i][c] (step-major, cand_stride columns); inactive and padding
 // candidates get zero coefficients (simulated harmlessly, never priced).
+// One candidate's FP32 row for mc_tile_kernel_f32 (kernels_mc.cu): the
+// coefficients {nu sqrt(dt), nu^2 dt / 2, rho sqrt(dt), srho sqrt(dt)} scaled
+// by log2(e) with the drift negated, {c1, -c2, rs, ss}; pairs: the
+// pair-interleaved layout of the packed FP32x2 kernel, per pair of
+// candidates {c1 c1' -c2 -c2'} {rs rs' ss ss'}.
+__device__ __forceinline__ void put_coef32(float4* __restrict__ coef32, int64_t step, int c, int cand_stride,
+                                           int pairs, const double4 v) {
+    constexpr double L = 1.4426950408889634;
+    const float a = static_cast<float>(v.x * L), b = static_cast<float>(-v.y * L);
+    const float r = static_cast<float>(v.z * L), q = static_cast<float>(v.w * L);
+    if (!pairs) {
+        coef32[step * cand_stride + c] = make_float4(a, b, r, q);
+        return;
+    }
+    float* row = reinterpret_cast<float*>(coef32 + step * cand_stride + (c & ~1));
+    const int h = c & 1;
+    row[h] = a;
+    row[2 + h] = b;
+    row[4 + h] = r;
+    row[6 + h] = q;
+}
+
 // idx: the compacted candidate list (t2_compact_kernel): candidate c of the
 // launch is chain idx[c] (-1: no candidate); n_live: the list's length - a
 // launch that starts past it writes nothing (its MC blocks all exit).
@@ -1460,7 +1482,8 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const int32_t
                                const int32_t n_local, const int32_t cand_stride,
                                const double* __restrict__ t_end, const double* __restrict__ dt,
                                const double* __restrict__ sdt, const int64_t total_steps,
-                               double4* __restrict__ coef, float4* __restrict__ coef32) {
+                               double4* __restrict__ coef, float4* __restrict__ coef32,
+                               const int pairs) {
     if (c0 >= *n_live) return;  // uniform
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<int64_t>(cand_stride) * total_steps) return;
@@ -1468,7 +1491,7 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const int32_t
     const int64_t i = t / cand_stride;
     const int32_t chain = c < n_local ? idx[c0 + c] : -1;
     if (chain < 0) {
-        if (coef32) coef32[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (coef32) put_coef32(coef32, i, c, cand_stride, pairs, make_double4(0.0, 0.0, 0.0, 0.0));
         else coef[t] = make_double4(0.0, 0.0, 0.0, 0.0);
         return;
     }
@@ -1482,8 +1505,7 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const int32_t
     const double srho = sqrt((0.0 < q) ? q : 0.0);
     const double s = sdt[i];
     const double4 v = make_double4(nu * s, 0.5 * nu * nu * dt[i], rho * s, srho * s);
-    if (coef32) coef32[t] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
-                                        static_cast<float>(v.z), static_cast<float>(v.w));
+    if (coef32) put_coef32(coef32, i, c, cand_stride, pairs, v);
     else coef[t] = v;
 }
 
@@ -1935,7 +1957,7 @@ cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int3
     if (n <= 0) return cudaSuccess;
     t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
         chains, idx, n_live, c0, n_local, cand_stride, t_end, dt, sdt, total_steps,
-        fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr);
+        fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr, fp32 == 2);
     return cudaGetLastError();
 }
 

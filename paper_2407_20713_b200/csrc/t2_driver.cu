@@ -221,7 +221,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
                 const int32_t nc = std::min(chunk, n_local - c0);
                 const int32_t nc_pad = (nc + cb - 1) / cb * cb;
                 check_cuda(launch_t2_coef(chains, cidx, n_live, c0, nc, nc_pad, d_tend, d_dt, d_sdt, S,
-                                          coef, fp32 ? 1 : 0, ctx->stream), "t2_coef");
+                                          coef, fp32 ? (cb >= 2 ? 2 : 1) : 0, ctx->stream), "t2_coef");
                 McParams Q = P;
                 Q.n_cand = nc;
                 Q.alpha0 = alpha0_c + c0;

@@ -44,7 +44,8 @@ def main(mode):
                                   precision=os.environ.get("SABR_PRECISION", "fp64"))
         r = eng.calibrate_case2_T2(surf, None, s, plan, fixed)
     elif mode == "mc":
-        plan = pkg.SimulationPlan(num_paths=1 << 20, seed=3, rng=os.environ.get("SABR_RNG", "xoshiro"))
+        plan = pkg.SimulationPlan(num_paths=1 << 20, seed=3, rng=os.environ.get("SABR_RNG", "xoshiro"),
+                                  precision=os.environ.get("SABR_PRECISION", "fp64"))
         p = pkg.StaticSabrParams(0.375162, 0.999999, 0.331441, -0.999999)
         r = eng.price_european_batch(p, 2257.37, [2257.37], 0.018196, 0.034516, 0.495890, plan)
     elif mode == "c5":
