@@ -670,6 +670,32 @@ SABR_HD void dynamic_quad_terms(double nu1_sq, double nu2_sq, double eta1, doubl
     c0 = fma(inv, B * T, inv);
 }
 
+// dynamic_quad_terms with 1/omega and omega supplied (beta fixed: alpha times
+// the CTA's 1 / f^(1-beta), f^(1-beta) times 1/alpha)
+SABR_HD void dynamic_quad_terms_r(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double beta,
+                                  double inv, double omega, double T, double& c0, double& a1, double& a2) {
+    const double omb = 1.0 - beta;
+    const double q = omb * inv;
+    const double p = q - eta1;
+    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
+    a1 = -0.5 * p;
+    a2 = fma(k * (1.0 / 24.0), omega, fma(0.25, p, (omb * q) * (1.0 / 12.0)));
+    const double B = fma(q * (1.0 / 24.0), q, fma((0.25 * beta) * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0)));
+    c0 = fma(inv, B * T, inv);
+}
+
+// dynamic_quad_terms_r at beta = 1 (f^(1-beta) = 1: 1/omega = alpha, omega =
+// rcp(alpha)): with 1 - beta = 0, q = 0 and p = -eta1, the same roundings as
+// the general form term by term (each dropped operand is an exact zero)
+SABR_HD void dynamic_quad_terms_b1(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double inv,
+                                   double omega, double T, double& c0, double& a1, double& a2) {
+    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
+    a1 = 0.5 * eta1;
+    a2 = fma(k * (1.0 / 24.0), omega, -0.25 * eta1);
+    const double B = fma(0.25 * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0));
+    c0 = fma(inv, B * T, inv);
+}
+
 #ifdef __CUDACC__
 // The Taylor tables of series_nu1 .. series_eta2 as one 64-double block
 // (4 series x 16, two trailing zeros each), for a shared-memory copy: FP64
@@ -731,13 +757,39 @@ __device__ __forceinline__ void case1_closed_pair(double x, const double2* __res
     }
 }
 
+// case1_closed_pair with 1/x supplied (ix, within a few ulp of the quotient):
+// the scale factors 6/x^3, 2/x^2 and 3/x^4 from it, the brackets unchanged
+template <int PAIR, int STRIDE = 1>
+__device__ __forceinline__ void case1_closed_pair_r(double x, double ix, const double2* __restrict__ tab,
+                                                    double& f, double& g) {
+    // exp(-x) for x >= 0.25 (never NaN: x = 2bT or (a+b)T from the box);
+    // past x = 700 the clamp's e ~ 1e-304 leaves every bracket the double it
+    // is with e = 0 (each bracket holds a term >= x - 1), so exp_tab's
+    // saturation selects are not needed
+    const double e = exp_tab_unsat<STRIDE>(fmax(-x, -700.0), tab);
+    if constexpr (PAIR == 0) {
+        const double x2 = SABR_MUL(x, x);
+        const double c6 = (6.0 * ix) * (ix * ix);
+        f = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), x), 1.0), e));
+        g = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(x, SABR_ADD(e, 1.0))));
+    } else {
+        const double r2 = ix * ix;
+        f = SABR_MUL(2.0 * r2, SABR_SUB(e, SABR_SUB(1.0, x)));
+        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
+                                     SABR_MUL(SABR_MUL(2.0, x), SABR_SUB(x, 3.0)));
+        g = SABR_MUL(3.0 * (r2 * r2), poly);
+    }
+}
+
 // One functional pair for C chains: when every chain of the thread takes the
 // same branch (the rule late in a schedule, when the chains cluster), their
 // evaluations share one branch body and interleave (C-fold ILP); mixed
 // threads evaluate chain by chain.  Per-chain results do not depend on C.
-template <int PAIR, int C, int STRIDE = 1>
+// RCP: the closed forms take 1/x from ix (case1_closed_pair_r)
+template <int PAIR, int C, int STRIDE = 1, bool RCP = false>
 __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
-                                             const double2* __restrict__ tab, double (&f)[C], double (&g)[C]) {
+                                             const double2* __restrict__ tab, double (&f)[C], double (&g)[C],
+                                             const double (&ix)[C]) {
     constexpr double kXSwitch = 0.25;  // analytics.cpp:21
     bool all_series = true, all_closed = true;
 #pragma unroll
@@ -750,11 +802,15 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
         for (int c = 0; c < C; ++c) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
     } else if (all_closed) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
+        for (int c = 0; c < C; ++c) {
+            if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], ix[c], tab, f[c], g[c]);
+            else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
+        }
     } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (x[c] < kXSwitch) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+            else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], ix[c], tab, f[c], g[c]);
             else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
         }
     }
@@ -765,17 +821,21 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
 // reference's quotients; they scale the cancelling brackets, they are not
 // inside them) and exp by table (exp_tab, ~0.5 ulp).  The brackets keep the
 // reference's operation order and roundings.
+// ixb, ixab: 1/(2bT) and 1/((a+b)T) as 1/(2b) * 1/T, 1/(a+b) * 1/T (the
+// scale factors of the closed forms, case1_closed_pair_r).
 __device__ __forceinline__ void dyn_coeffs_case1_fast(double rho0, double nu0, double a, double b, double T,
+                                                      double ixb, double ixab,
                                                       const double* __restrict__ ser,
                                                       const double2* __restrict__ tab, double& nu1_sq,
                                                       double& nu2_sq, double& eta1, double& eta2_sq) {
     const double xb[1] = {SABR_MUL(SABR_MUL(2.0, b), T)};
     const double xab[1] = {SABR_MUL(SABR_ADD(a, b), T)};
+    const double rb[1] = {ixb}, rab[1] = {ixab};
     const double nn = SABR_MUL(nu0, nu0);
     const double nr = SABR_MUL(nu0, rho0);
     double f1[1], f2[1], g1[1], g2[1];
-    case1_pair_n<0, 1>(xb, ser, tab, f1, f2);
-    case1_pair_n<1, 1>(xab, ser, tab, g1, g2);
+    case1_pair_n<0, 1, 1, true>(xb, ser, tab, f1, f2, rb);
+    case1_pair_n<1, 1, 1, true>(xab, ser, tab, g1, g2, rab);
     nu1_sq = SABR_MUL(nn, f1[0]);
     nu2_sq = SABR_MUL(nn, f2[0]);
     eta1 = SABR_MUL(nr, g1[0]);

@@ -261,6 +261,7 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
     a.free_mask = free_mask;
     a.fast = single_reflection(a, dim_full) ? 1 : 0;
     a.fast_free = single_reflection(a, dim_full, true) ? 1 : 0;
+    a.beta_one = (dim_full > 1 && !((free_mask >> 1) & 1u) && start_full[1] == 1.0) ? 1 : 0;
     a.dim_full = dim_full;
     a.chain_length = sch.chain_length;
     a.builtin = builtin;

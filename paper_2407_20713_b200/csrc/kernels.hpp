@@ -78,6 +78,7 @@ struct SaLevelArgs {
     int32_t nranks;
     int32_t fast;                // all dims free and one reflection always lands in the box
     int32_t fast_free;           // one reflection always lands in the box for every searched dim
+    int32_t beta_one;            // Case I: beta (dim 1) not searched and held at exactly 1
     double t0;
     uint64_t seed;
     int64_t chain_begin;         // global index of this rank's first chain

@@ -387,10 +387,11 @@ struct QGrid {
     const double* R;    // [ns][kQrStride], 16-byte aligned
     const double* ser;  // [4][kSeriesStride] Case I series tables (horner_s)
     const double2* tab;
+    const double* iT;   // [ns] 1 / T (Case I: the closed forms' 1/x = 1/(2b) * 1/T)
 };
 
 __host__ __device__ inline size_t qstage_bytes(int ns) {
-    return sizeof(double) * (4 * kSeriesStride + static_cast<size_t>(kQrStride + 3) * ns);
+    return sizeof(double) * (4 * kSeriesStride + static_cast<size_t>(kQrStride + 4) * ns);
 }
 
 __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
@@ -404,6 +405,7 @@ __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
         d[i] = sv.T[i];
         d[ns + i] = sv.lnf_hi[i];
         d[2 * ns + i] = sv.lnf_lo[i];
+        d[3 * ns + i] = 1.0 / sv.T[i];
     }
     __syncthreads();
     QGrid g;
@@ -413,6 +415,7 @@ __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
     g.T = d;
     g.lnf_hi = d + ns;
     g.lnf_lo = d + 2 * ns;
+    g.iT = d + 3 * ns;
     g.tab = nullptr;
     return g;
 }
@@ -446,16 +449,19 @@ __device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
     return qr_cost(static_qterms(v, pw, g.T[0]), load_qr(g.R));
 }
 
+// The Case I objective of one vector (case1_cost_n's arithmetic, bit for bit).
 __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
     double sum = 0.0;
     const double omb = 1.0 - v[1];
+    const double rb = fast_rcp(SABR_MUL(2.0, v[5])), rab = fast_rcp(SABR_ADD(v[4], v[5]));
+    const double ia = fast_rcp(v[0]);
     for (int i = 0; i < g.ns; ++i) {
-        const double T = g.T[i];
+        const double T = g.T[i], iT = g.iT[i];
         double n1, n2, e1, e2;
-        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, g.ser, g.tab, n1, n2, e1, e2);
+        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, rb * iT, rab * iT, g.ser, g.tab, n1, n2, e1, e2);
         const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
         QuadTerms t;
-        dynamic_quad_terms(n1, n2, e1, e2, v[0], v[1], pw, T, t.c0, t.a1, t.a2);
+        dynamic_quad_terms_r(n1, n2, e1, e2, v[1], v[0] * fast_rcp(pw), pw * ia, T, t.c0, t.a1, t.a2);
         sum += qr_cost(t, load_qr(g.R + kQrStride * i));
     }
     return sum;
@@ -483,22 +489,51 @@ __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const 
 // pw_fixed: when beta is not searched, f_i^(1-beta) per slice, computed once
 // per CTA with the same pow_fwd (so the values are the ones each chain would
 // compute); nullptr when beta is free.
-template <int C, int DIMF, int STRIDE = 1>
+// slices whose f^(1-beta) a CTA keeps when beta is not searched (pw_fixed)
+constexpr int kMaxPwSlices = 64;
+
+// BETA1: beta is held at exactly 1 (C3), f^(1-beta) = 1 (dynamic_quad_terms_b1).
+template <int C, int DIMF, int STRIDE = 1, bool BETA1 = false>
 __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const QGrid& g,
                                              double (&out)[C], const double* pw_fixed = nullptr,
                                              const double2* tab = nullptr) {
     if (STRIDE == 1) tab = g.tab;
+    // Reciprocals shared by the slices (r02): the closed forms scale their
+    // brackets by 6/x^3 (x = 2bT), 2/x^2 and 3/x^4 (x = (a+b)T); with
+    // 1/x = 1/(2b) * 1/T and 1/((a+b)T) = 1/(a+b) * 1/T (1/T staged per CTA)
+    // two reciprocals per chain replace three per slice.  1/omega =
+    // alpha * rcp(f^(1-beta)) and omega = f^(1-beta) * rcp(alpha): one
+    // reciprocal of alpha per chain, and with beta fixed the CTA's
+    // rcp(f^(1-beta)) per slice.  Each factor is within a few ulp of the
+    // per-slice quotient; it scales a cancelling bracket, it is not inside
+    // one (the brackets keep the reference's operations, analytics.cpp:47-67).
+    // per chain, slice-independent: 2b, a+b, their reciprocals, rcp(alpha),
+    // nu0^2, nu0 rho0, (nu0 rho0)^2
+    double b2[C], ab[C], rb[C], rab[C], ia[C], nn[C], nr[C], nr2[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        b2[c] = SABR_MUL(2.0, v[c][5]);
+        ab[c] = SABR_ADD(v[c][4], v[c][5]);
+        rb[c] = fast_rcp(b2[c]);
+        rab[c] = fast_rcp(ab[c]);
+        ia[c] = fast_rcp(v[c][0]);
+        nn[c] = SABR_MUL(v[c][3], v[c][3]);
+        nr[c] = SABR_MUL(v[c][3], v[c][2]);
+        nr2[c] = SABR_MUL(nr[c], nr[c]);
+    }
 #pragma unroll
     for (int c = 0; c < C; ++c) out[c] = 0.0;
     for (int i = 0; i < g.ns; ++i) {
-        const double T = g.T[i];
+        const double T = g.T[i], iT = g.iT[i];
         const QrFactor f = load_qr(g.R + kQrStride * i);
         // dyn_coeffs_case1_fast for the C chains, branch bodies shared
-        double xb[C], xab[C], f1[C], f2[C], g1[C], g2[C];
+        double xb[C], xab[C], ixb[C], ixab[C], f1[C], f2[C], g1[C], g2[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            xb[c] = SABR_MUL(SABR_MUL(2.0, v[c][5]), T);
-            xab[c] = SABR_MUL(SABR_ADD(v[c][4], v[c][5]), T);
+            xb[c] = SABR_MUL(b2[c], T);
+            xab[c] = SABR_MUL(ab[c], T);
+            ixb[c] = rb[c] * iT;
+            ixab[c] = rab[c] * iT;
         }
         // both functional pairs of every chain in the closed-form regime (the
         // rule on C3's surfaces): one straight-line block, 2C independent
@@ -509,20 +544,31 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
         if (all_closed) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                case1_closed_pair<0, STRIDE>(xb[c], tab, f1[c], f2[c]);
-                case1_closed_pair<1, STRIDE>(xab[c], tab, g1[c], g2[c]);
+                case1_closed_pair_r<0, STRIDE>(xb[c], ixb[c], tab, f1[c], f2[c]);
+                case1_closed_pair_r<1, STRIDE>(xab[c], ixab[c], tab, g1[c], g2[c]);
             }
         } else {
-            case1_pair_n<0, C, STRIDE>(xb, g.ser, tab, f1, f2);
-            case1_pair_n<1, C, STRIDE>(xab, g.ser, tab, g1, g2);
+            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, ixb);
+            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, ixab);
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            const double nn = SABR_MUL(v[c][3], v[c][3]), nr = SABR_MUL(v[c][3], v[c][2]);
-            const double pw = pw_fixed ? pw_fixed[i] : pow_fwd<true, STRIDE>(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], tab);
             QuadTerms t;
-            dynamic_quad_terms(SABR_MUL(nn, f1[c]), SABR_MUL(nn, f2[c]), SABR_MUL(nr, g1[c]),
-                               SABR_MUL(SABR_MUL(nr, nr), g2[c]), v[c][0], v[c][1], pw, T, t.c0, t.a1, t.a2);
+            const double n1 = SABR_MUL(nn[c], f1[c]), n2 = SABR_MUL(nn[c], f2[c]);
+            const double e1 = SABR_MUL(nr[c], g1[c]), e2 = SABR_MUL(nr2[c], g2[c]);
+            if constexpr (BETA1) {
+                dynamic_quad_terms_b1(n1, n2, e1, e2, v[c][0], ia[c], T, t.c0, t.a1, t.a2);
+            } else {
+                double pw, ipw;
+                if (pw_fixed) {
+                    pw = pw_fixed[i];
+                    ipw = pw_fixed[kMaxPwSlices + i];
+                } else {
+                    pw = pow_fwd<true, STRIDE>(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], tab);
+                    ipw = fast_rcp(pw);
+                }
+                dynamic_quad_terms_r(n1, n2, e1, e2, v[c][1], v[c][0] * ipw, pw * ia[c], T, t.c0, t.a1, t.a2);
+            }
             out[c] += qr_cost(t, f);
         }
     }
@@ -943,7 +989,6 @@ template <int C>
 constexpr int level_nt() { return C == 3 ? 32 : kLevelThreads / C; }
 template <int C>
 constexpr int level_min_ctas() { return C == 3 ? 8 : kPairMinCtas; }
-constexpr int kMaxPwSlices = 64;
 // copies of the bank-replicated exp table (device_common.cuh: kExpRep) per
 // objective in the C-chain level kernel
 template <int KIND>
@@ -962,7 +1007,8 @@ constexpr int rep_copies() { return KIND == OBJ_STATIC ? kExpRep : 4; }
 // FIXM (with ALLFREE false): a compile-time mask of fixed coordinates, every
 // other coordinate searched with the one-reflection propose (a.fast_free);
 // Case I with beta fixed, the C3 configuration, uses FIXM = 2.
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT, bool PIPE = false, int FIXM = 0>
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int NT, bool PIPE = false, int FIXM = 0,
+          bool B1 = false>
 __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const ObjGrid<GK>& g,
                                                  const double2* tab_s, const double2* tab_lane,
                                                  const double* pw_fixed,
@@ -1061,7 +1107,7 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
                 else static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
             } else if constexpr (GK == kGridQR) {
                 if (tab_lane) case1_cost_n<C, DIMF, rep_copies<KIND>()>(y, g, fy, pw_fixed, tab_lane);
-                else case1_cost_n<C, DIMF>(y, g, fy, pw_fixed);
+                else case1_cost_n<C, DIMF, 1, B1>(y, g, fy, pw_fixed);
             }
             else case1_cost_n<C, DIMF>(y, g, fy);
             // Metropolis (annealer.cpp:125-126) without a branch: the FP32
@@ -1138,7 +1184,9 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
     __syncthreads();
 }
 
-template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int FIXM = 0, bool PIPE = false>
+// B1 (with FIXM bit 1): beta held at exactly 1 (SaLevelArgs::beta_one), the
+// Case I objective without f^(1-beta) (case1_cost_n BETA1)
+template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int FIXM = 0, bool PIPE = false, bool B1 = false>
 __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
@@ -1186,18 +1234,21 @@ __global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
     pdl_wait();
     if (st->done) return;  // early-stopped run (max_evals): uniform exit
     // Case I with beta not searched: f_i^(1-beta) is one value per slice
-    __shared__ double pw_s[kMaxPwSlices];
+    __shared__ double pw_s[2 * kMaxPwSlices];  // f_i^(1-beta), then rcp(f_i^(1-beta))
     const double* pw_fixed = nullptr;
     if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
         if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {
             const double omb = 1.0 - st->incumbent[1];
-            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            for (int i = threadIdx.x; i < g.ns; i += NT) {
+                pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+                pw_s[kMaxPwSlices + i] = fast_rcp(pw_s[i]);
+            }
             __syncthreads();
             pw_fixed = pw_s;
         }
     }
-    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT, PIPE, FIXM>(a, g, tab_s, tab_lane, pw_fixed, st, temp,
-                                                                 inv_temp, active, chain, rng, bp_s, rs, rec);
+    run_level_chains<KIND, DIMF, ALLFREE, GK, C, NT, PIPE, FIXM, B1>(a, g, tab_s, tab_lane, pw_fixed, st, temp,
+                                                                     inv_temp, active, chain, rng, bp_s, rs, rec);
     if (!publish_block_record<NT, DIMF>(rs, rec, a)) return;
     reduce_block_records<NT, DIMF>(rs, a, level);
 }
@@ -1220,7 +1271,7 @@ __global__ void __launch_bounds__(kLevelThreads / C, 1)
     __shared__ sabr_level_record rec;
     __shared__ double2 tab_s[kExpTableSize];
     __shared__ double bp_s[C][DIMF][NT];
-    __shared__ double pw_s[kMaxPwSlices];
+    __shared__ double pw_s[2 * kMaxPwSlices];  // f_i^(1-beta), then rcp(f_i^(1-beta))
     sabr_sa_state* st = a.state;
     stage_exp(sv, tab_s);
     ObjGrid<GK> g = stage_obj<GK>(sv, smem);
@@ -1238,7 +1289,10 @@ __global__ void __launch_bounds__(kLevelThreads / C, 1)
     if constexpr (KIND == OBJ_CASE1 && GK == kGridQR) {
         if (!((a.free_mask >> 1) & 1u) && g.ns <= kMaxPwSlices) {  // beta not searched: constant
             const double omb = 1.0 - st->incumbent[1];
-            for (int i = threadIdx.x; i < g.ns; i += NT) pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+            for (int i = threadIdx.x; i < g.ns; i += NT) {
+                pw_s[i] = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
+                pw_s[kMaxPwSlices + i] = fast_rcp(pw_s[i]);
+            }
             __syncthreads();
             pw_fixed = pw_s;
         }
@@ -1754,7 +1808,8 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
                 if (gk == kGridQR && cpt == 2 && !all_free && a.fast_free != 0 &&
                     a.free_mask == ((1u << DIMF) - 1u & ~2u))
                     k = pipe_enabled() ? sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, true>
-                                       : sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, false>;
+                        : a.beta_one     ? sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, false, true>
+                                         : sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, false>;
             }
             const int ntc = gk == kGridQR && cpt == 3 ? 3 : (gk == kGridQR && cpt == 1 ? 1 : 2);
             const unsigned threads = static_cast<unsigned>(ntc == 3 ? level_nt<3>() : ntc == 1 ? level_nt<1>() : level_nt<2>());
