@@ -588,35 +588,64 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
     }
 }
 
-// reduce_payoffs (mc.cpp:146-157) over the tiles, in tile order.
-__global__ void mc_reduce_kernel(const McParams P, double* __restrict__ value,
-                                 double* __restrict__ std_error) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= static_cast<int64_t>(P.n_cand) * P.n_quotes) return;
-    const int c = static_cast<int>(t / P.n_quotes);
-    if (P.active != nullptr && P.active[c] == 0) return;
-    // tiles in fixed order (tile-major partials: coalesced over (c, q))
-    const int64_t stride = static_cast<int64_t>(P.n_cand) * P.n_quotes * 2;
-    const double* p = P.partials + t * 2;
-    // unrolled so 16 tiles' loads are in flight per round trip (the same
-    // sequential order of additions: the loop was latency-bound, one L2 round
-    // trip per tile, 0.3 ms per C4 step)
+// reduce_payoffs (mc.cpp:146-157) over the tiles.  Block (X, G): threadIdx.x
+// picks one of X consecutive (candidate, quote) columns (coalesced: the
+// partials are tile-major), threadIdx.y one of G tile groups; group y sums
+// tiles y, y + G, y + 2G, ... in order, then the G group sums are added in
+// group order.  G depends only on n_tiles (a function of num_paths and ppt),
+// so a price is still a pure function of the plan.  r02: with one thread per
+// column (G = 1) C4's 672 columns ran as 6 CTAs walking 782 tiles each, 88 us
+// per SA step, latency-bound; G = 32 spreads the walk over 32x the threads
+// (a single-candidate price of 2^24 paths: 32768 tiles, G = 256).
+constexpr int kReduceThreads = 256;
+__host__ __device__ inline int reduce_groups(int n_tiles) {
+    int g = 1;
+    while (g < kReduceThreads && g * 2 * 24 <= n_tiles) g *= 2;  // >= 24 tiles per group
+    return g;
+}
+
+__global__ void __launch_bounds__(kReduceThreads) mc_reduce_kernel(const McParams P, double* __restrict__ value,
+                                                                   double* __restrict__ std_error) {
+    __shared__ double2 part[kReduceThreads];
+    const int G = blockDim.y, X = blockDim.x;
+    const int64_t ncol = static_cast<int64_t>(P.n_cand) * P.n_quotes;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * X + threadIdx.x;
+    const bool on = t < ncol && (P.active == nullptr || P.active[t / P.n_quotes] != 0);
+    const int64_t stride = ncol * 2;
     double s1 = 0.0, s2 = 0.0;
-    int k = 0;
-    for (; k + 16 <= P.n_tiles; k += 16) {
-        double2 v[16];
+    if (on) {
+        const double* p = P.partials + t * 2;
+        int k = threadIdx.y;
+        // 8 tiles' loads in flight per round trip, the additions in tile order
+        for (; k + 7 * G < P.n_tiles; k += 8 * G) {
+            double2 v[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = *reinterpret_cast<const double2*>(p + (k + u) * stride);
+            for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double2*>(p + (k + u * G) * stride);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            s1 += v[u].x;
-            s2 += v[u].y;
+            for (int u = 0; u < 8; ++u) {
+                s1 += v[u].x;
+                s2 += v[u].y;
+            }
+        }
+        for (; k < P.n_tiles; k += G) {
+            const double2 v = *reinterpret_cast<const double2*>(p + k * stride);
+            s1 += v.x;
+            s2 += v.y;
         }
     }
-    for (; k < P.n_tiles; ++k) {
-        s1 += p[k * stride];
-        s2 += p[k * stride + 1];
+    if (G > 1) {
+        part[threadIdx.y * X + threadIdx.x] = make_double2(s1, s2);
+        __syncthreads();
+        if (threadIdx.y != 0) return;
+        s1 = 0.0;
+        s2 = 0.0;
+        for (int y = 0; y < G; ++y) {
+            const double2 v = part[y * X + threadIdx.x];
+            s1 += v.x;
+            s2 += v.y;
+        }
     }
+    if (!on) return;
     const double n = static_cast<double>(P.num_paths);
     const double mean = s1 / n;
     const double q = (s2 - n * mean * mean) / (n - 1.0);
@@ -753,7 +782,8 @@ cudaError_t launch_mc_reduce(const McParams& p, double* value, double* std_error
                              const double* market, double* cost, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(p.n_cand) * p.n_quotes;
     if (n > 0) {
-        mc_reduce_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(p, value, std_error);
+        const int G = reduce_groups(p.n_tiles), X = kReduceThreads / G;
+        mc_reduce_kernel<<<static_cast<unsigned>((n + X - 1) / X), dim3(X, G), 0, s>>>(p, value, std_error);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
