@@ -31,12 +31,70 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Per-warp payoff sums by a shared-memory transpose (both tile kernels, r02): each
+// lane writes its discounted payoffs and their squares for 16 (candidate,
+// quote, moment) columns as one row of a [32][17] tile; then the two
+// half-warps each sum 16 rows of one column and meet with one shuffle.  Per
+// value that is one STS, one LDS and one DADD, where two 5-level warp_sum
+// trees cost ten shuffles and five DADD; the order (lanes 0-15 and 16-31 in
+// four interleaved partial sums each, then the halves) is fixed, so a price
+// still depends only on (num_paths, ppt).
+constexpr int kTrCols = 16;
+constexpr int kTrStride = kTrCols + 1;  // 64-bit rows 17 doubles apart: no bank conflicts
+
+__device__ __forceinline__ void tr_flush(double* __restrict__ tb, double* __restrict__ accw, int base,
+                                         int ncols, int lane) {
+    __syncwarp();
+    const int col = lane & (kTrCols - 1), r0 = lane & kTrCols;  // rows 0-15 or 16-31
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < kTrCols; r += 4) {
+        s0 += tb[(r0 + r) * kTrStride + col];
+        s1 += tb[(r0 + r + 1) * kTrStride + col];
+        s2 += tb[(r0 + r + 2) * kTrStride + col];
+        s3 += tb[(r0 + r + 3) * kTrStride + col];
+    }
+    double s = (s0 + s1) + (s2 + s3);
+    const double o = __shfl_xor_sync(0xffffffffu, s, kTrCols);
+    s = (lane < kTrCols) ? s + o : o + s;  // the same sum on both halves
+    if (lane < ncols) accw[base + lane] += s;
+    __syncwarp();
+}
+
+// Discounted call payoffs of one path for every (candidate, quote), mc.cpp:265-269,
+// added to the warp's accumulators accw[(cc * mq + j) * 2 + {0, 1}].
+template <int CB>
+__device__ __forceinline__ void payoff_sums_tr(const double (&F)[CB], bool live, uint32_t act_mask,
+                                               const double* __restrict__ K, int mq, double disc,
+                                               double* __restrict__ tb, double* __restrict__ accw,
+                                               int lane) {
+    double* row = tb + lane * kTrStride;
+    int col = 0, base = 0;
+#pragma unroll
+    for (int cc = 0; cc < CB; ++cc) {
+        const bool on = live && ((act_mask >> cc) & 1u);
+        for (int j = 0; j < mq; ++j) {
+            const double d = F[cc] - __ldg(K + j);
+            const double v = on ? disc * ((d < 0.0) ? 0.0 : d) : 0.0;
+            row[col] = v;
+            row[col + 1] = v * v;
+            col += 2;
+            if (col == kTrCols) {
+                tr_flush(tb, accw, base, kTrCols, lane);
+                base += kTrCols;
+                col = 0;
+            }
+        }
+    }
+    if (col > 0) tr_flush(tb, accw, base, col, lane);
+}
+
 // CONST: every slice of the launch has time-invariant step rows (McSlice::
 // const_coef): the first row and dt serve every step, no per-step loads.  A
 // separate instantiation, so the general kernel's code is unchanged.
 template <int CB, bool CONST>
 __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_constant__ McParams P) {
-    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2]
+    extern __shared__ __align__(16) double acc[];  // [kWarps][CB][mq][2], then [kWarps][32][kTrStride]
 
     int64_t idx = blockIdx.x;
     const int tile = P.tile_begin + static_cast<int>(idx % P.tile_count);
@@ -192,23 +250,9 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
         }
         if (P.terminals != nullptr && live) P.terminals[path] = F[0];
         if (!reduce) continue;
-        // discounted call payoffs, mc.cpp:265-269, reduced over the warp
-        for (int j = 0; j < mq; ++j) {
-            const double K = __ldg(P.strikes + sl.q_begin + j);
-#pragma unroll
-            for (int cc = 0; cc < CB; ++cc) {
-                if (!((act_mask >> cc) & 1u)) continue;
-                const double d = F[cc] - K;
-                const double v = live ? sl.discount * ((d < 0.0) ? 0.0 : d) : 0.0;
-                const double s1 = warp_sum(v);
-                const double s2 = warp_sum(v * v);
-                if (lane == 0) {
-                    double* slot = acc + ((warp * CB + cc) * mq + j) * 2;
-                    slot[0] += s1;
-                    slot[1] += s2;
-                }
-            }
-        }
+        // discounted call payoffs, mc.cpp:265-269, summed over the warp
+        payoff_sums_tr<CB>(F, live, act_mask, P.strikes + sl.q_begin, mq, sl.discount,
+                           acc + kWarps * CB * mq * 2 + warp * 32 * kTrStride, acc + warp * CB * mq * 2, lane);
     }
     if (!reduce) return;
     __syncthreads();
@@ -226,64 +270,6 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
         out[0] = s1;
         out[1] = s2;
     }
-}
-
-// Per-warp payoff sums by a shared-memory transpose (FP32 kernel, r02): each
-// lane writes its discounted payoffs and their squares for 16 (candidate,
-// quote, moment) columns as one row of a [32][17] tile; then the two
-// half-warps each sum 16 rows of one column and meet with one shuffle.  Per
-// value that is one STS, one LDS and one DADD, where two 5-level warp_sum
-// trees cost ten shuffles and five DADD; the order (lanes 0-15 and 16-31 in
-// four interleaved partial sums each, then the halves) is fixed, so a price
-// still depends only on (num_paths, ppt).
-constexpr int kTrCols = 16;
-constexpr int kTrStride = kTrCols + 1;  // 64-bit rows 17 doubles apart: no bank conflicts
-
-__device__ __forceinline__ void tr_flush(double* __restrict__ tb, double* __restrict__ accw, int base,
-                                         int ncols, int lane) {
-    __syncwarp();
-    const int col = lane & (kTrCols - 1), r0 = lane & kTrCols;  // rows 0-15 or 16-31
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int r = 0; r < kTrCols; r += 4) {
-        s0 += tb[(r0 + r) * kTrStride + col];
-        s1 += tb[(r0 + r + 1) * kTrStride + col];
-        s2 += tb[(r0 + r + 2) * kTrStride + col];
-        s3 += tb[(r0 + r + 3) * kTrStride + col];
-    }
-    double s = (s0 + s1) + (s2 + s3);
-    const double o = __shfl_xor_sync(0xffffffffu, s, kTrCols);
-    s = (lane < kTrCols) ? s + o : o + s;  // the same sum on both halves
-    if (lane < ncols) accw[base + lane] += s;
-    __syncwarp();
-}
-
-// Discounted call payoffs of one path for every (candidate, quote), mc.cpp:265-269,
-// added to the warp's accumulators accw[(cc * mq + j) * 2 + {0, 1}].
-template <int CB>
-__device__ __forceinline__ void payoff_sums_tr(const double (&F)[CB], bool live, uint32_t act_mask,
-                                               const double* __restrict__ K, int mq, double disc,
-                                               double* __restrict__ tb, double* __restrict__ accw,
-                                               int lane) {
-    double* row = tb + lane * kTrStride;
-    int col = 0, base = 0;
-#pragma unroll
-    for (int cc = 0; cc < CB; ++cc) {
-        const bool on = live && ((act_mask >> cc) & 1u);
-        for (int j = 0; j < mq; ++j) {
-            const double d = F[cc] - __ldg(K + j);
-            const double v = on ? disc * ((d < 0.0) ? 0.0 : d) : 0.0;
-            row[col] = v;
-            row[col + 1] = v * v;
-            col += 2;
-            if (col == kTrCols) {
-                tr_flush(tb, accw, base, kTrCols, lane);
-                base += kTrCols;
-                col = 0;
-            }
-        }
-    }
-    if (col > 0) tr_flush(tb, accw, base, col, lane);
 }
 
 // The FP32 fast path (SABR_FP32): the same streams, the reference's log-Euler
@@ -682,15 +668,17 @@ __global__ void mc_cost_kernel(const McParams P, const double* __restrict__ valu
 template <int CB>
 cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     const int mq = p.max_q;
-    // FP32: the warps' payoff transpose tiles follow the accumulators (payoff_sums_tr)
+    // the warps' payoff transpose tiles follow the accumulators (payoff_sums_tr)
     const size_t smem = p.partials ? (static_cast<size_t>(kWarps) * CB * mq * 2 +
-                                      (p.fp32 ? static_cast<size_t>(kWarps) * 32 * kTrStride : 0)) * sizeof(double)
+                                      static_cast<size_t>(kWarps) * 32 * kTrStride) * sizeof(double)
                                    : 0;
     bool cst = p.n_slices > 0;
     for (int i = 0; i < p.n_slices; ++i) cst = cst && p.host_slices != nullptr && p.host_slices[i].const_coef;
     auto k = p.fp32 ? (cst ? mc_tile_kernel_f32<CB, true> : mc_tile_kernel_f32<CB, false>)
                     : (cst ? mc_tile_kernel<CB, true> : mc_tile_kernel<CB, false>);
-    if (smem > 48 * 1024) {
+    // the FP64 kernel's 22 KB of static tables leave 26 KB of dynamic shared
+    // memory by default: opt in to the size this launch needs
+    if (smem > 16 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
