@@ -502,6 +502,14 @@ def secondary(eng, torch, dev, stream, peaks):
             "precision": precision, "seconds": secs, "final_cost": rep.final_cost,
             "sample": "one SA step (L=1, one level) of 2048 chains; C5 names 1e6 chains over 8 GPUs "
                       "(125000 per GPU, ~61x this sample per GPU-step)"}
+        kps = t.path_steps / (t.kernel_ms / 1e3)
+        k5 = "c5_mc_calibration" + ("" if precision == "fp64" else "_fp32")
+        if precision == "fp64":
+            out[k5]["roofline"] = pipe_roofline(kps, per.get("c5_fp64_pipe_instr_per_candidate_path_step"),
+                                                fp64_lane_peak, "fp64", src)
+        else:
+            out[k5]["roofline"] = pipe_roofline(kps, per.get("c5_fp32_xu_instr_per_candidate_path_step"),
+                                                peaks["mufu_tops"], "xu (MUFU)", src)
     # MC European pricing in the paper's shape (SSabr, 2^24 paths, 123 + 1 steps of
     # 1/250 to T = 0.4959), through price_european_batch; the paper's GTX470 did 2.18e8 (FP64) and
     # 1.62e9 (FP32) path-steps/s on this workload
@@ -524,6 +532,10 @@ def secondary(eng, torch, dev, stream, peaks):
         if precision == "fp64":
             out["mc_european_pricing"]["roofline"] = pipe_roofline(
                 ps / secs, per.get("mc_single_fp64_pipe_instr_per_path_step"), fp64_lane_peak, "fp64",
+                src + " (whole call: simulate + reduce)")
+        else:
+            out["mc_european_pricing_fp32"]["roofline"] = pipe_roofline(
+                ps / secs, per.get("mc_single_fp32_xu_instr_per_path_step"), peaks["mufu_tops"], "xu (MUFU)",
                 src + " (whole call: simulate + reduce)")
     # C1 (BASELINE.json configs[0]): the reference's own CPU-sized case, static T_I on one EURO STOXX 50
     # slice with the acceptance schedule (32 chains, 412 levels, 1,000,001 evals): latency-bound on a GPU
@@ -562,6 +574,9 @@ def secondary(eng, torch, dev, stream, peaks):
             "bound": "fp64", "achieved": a, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": a / peaks["fp64_tflops"], "flops_per_eval": per["c3_flops_per_eval"],
             "source": "ncu DFMA x2 + DADD + DMUL per eval (profiles/fp64_per_eval.json), whole calibration"}
+        if per.get("c3_fp64_pipe_instr_per_eval"):
+            out["c3_case1_calibration"]["roofline"]["fp64_pipe"] = pipe_roofline(
+                (rep.evals - 1) / secs, per["c3_fp64_pipe_instr_per_eval"], fp64_lane_peak, "fp64", src)
     return out
 
 

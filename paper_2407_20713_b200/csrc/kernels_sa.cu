@@ -985,14 +985,19 @@ constexpr int kPairMinCtas = 11;
 // threads per CTA and CTAs per SM (launch bound) of the C-chain level kernel:
 // C = 1, 2 cover kLevelThreads chains per CTA; C = 3 (SABR_SA_CPT=3, A/B)
 // uses one warp of 96 chains and 8 CTAs per SM (<= 255 registers)
-template <int C>
-constexpr int level_nt() { return C == 3 ? 32 : kLevelThreads / C; }
-template <int C>
-constexpr int level_min_ctas() { return C == 3 ? 8 : kPairMinCtas; }
+// Case I with two chains per thread (r02): two-warp CTAs of 128 chains, 6 per
+// SM at 168 registers, so each CTA has room for the 8-copy bank-replicated exp
+// table (16 KB; 11 one-warp CTAs per SM could not hold it) and its 8 exp
+// lookups per eval stop conflicting (ncu r02d: 14.9M excess shared wavefronts
+// per level with one copy)
+template <int KIND, int C>
+constexpr int level_nt() { return C == 3 ? 32 : (KIND == OBJ_CASE1 && C == 2) ? 64 : kLevelThreads / C; }
+template <int KIND, int C>
+constexpr int level_min_ctas() { return C == 3 ? 8 : (KIND == OBJ_CASE1 && C == 2) ? 6 : kPairMinCtas; }
 // copies of the bank-replicated exp table (device_common.cuh: kExpRep) per
 // objective in the C-chain level kernel
 template <int KIND>
-constexpr int rep_copies() { return KIND == OBJ_STATIC ? kExpRep : 4; }
+constexpr int rep_copies() { return kExpRep; }
 
 // The chains of one CTA for one level (annealer.cpp:107-139) and the CTA's
 // level-end arg-min (annealer.cpp:141-159): on return (all threads) rs holds
@@ -1106,7 +1111,7 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
                 if (tab_lane) static_cost_n<C, DIMF, ALLFREE, rep_copies<KIND>()>(y, sl, tab_lane, fy);
                 else static_cost_n<C, DIMF, ALLFREE>(y, sl, tab_s, fy);
             } else if constexpr (GK == kGridQR) {
-                if (tab_lane) case1_cost_n<C, DIMF, rep_copies<KIND>()>(y, g, fy, pw_fixed, tab_lane);
+                if (tab_lane) case1_cost_n<C, DIMF, rep_copies<KIND>(), B1>(y, g, fy, pw_fixed, tab_lane);
                 else case1_cost_n<C, DIMF, 1, B1>(y, g, fy, pw_fixed);
             }
             else case1_cost_n<C, DIMF>(y, g, fy);
@@ -1187,16 +1192,13 @@ __device__ __forceinline__ void run_level_chains(const SaLevelArgs& a, const Obj
 // B1 (with FIXM bit 1): beta held at exactly 1 (SaLevelArgs::beta_one), the
 // Case I objective without f^(1-beta) (case1_cost_n BETA1)
 template <int KIND, int DIMF, bool ALLFREE, int GK, int C, int FIXM = 0, bool PIPE = false, bool B1 = false>
-__global__ void __launch_bounds__(level_nt<C>(), level_min_ctas<C>())
+__global__ void __launch_bounds__(level_nt<KIND, C>(), level_min_ctas<KIND, C>())
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
-    constexpr int NT = level_nt<C>();
-    // the static objective's pow reads the bank-replicated exp table
-    // (Case I: 8 copies would take 22 KB per CTA and push its 1563 one-warp
-    // CTAs out of one wave; 4 copies halve the conflicts, 1.93x the ideal
-    // wavefronts, but the kernel is bound by FP64 dependency latency and ran
-    // no faster: ncu r02, 649 vs 656 us per level, so Case I keeps one copy)
-    constexpr bool kRep = GK == kGridQR && KIND == OBJ_STATIC;
+    constexpr int NT = level_nt<KIND, C>();
+    // the static objective's pow and the Case I closed forms' exp read the
+    // bank-replicated exp table (Case I: two-warp CTAs, level_nt)
+    constexpr bool kRep = GK == kGridQR && (KIND == OBJ_STATIC || (KIND == OBJ_CASE1 && C == 2));
     constexpr int kRepN = rep_copies<KIND>();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
@@ -1812,7 +1814,8 @@ cudaError_t level_t(const SurfaceView& sv, const SaLevelArgs& a, int64_t level, 
                                          : sa_level_multi_kernel<KIND, DIMF, false, kGridQR, 2, 2, false>;
             }
             const int ntc = gk == kGridQR && cpt == 3 ? 3 : (gk == kGridQR && cpt == 1 ? 1 : 2);
-            const unsigned threads = static_cast<unsigned>(ntc == 3 ? level_nt<3>() : ntc == 1 ? level_nt<1>() : level_nt<2>());
+            const unsigned threads = static_cast<unsigned>(ntc == 3 ? level_nt<KIND, 3>()
+                                                           : ntc == 1 ? level_nt<KIND, 1>() : level_nt<KIND, 2>());
             const unsigned grid = static_cast<unsigned>((a.n_local + threads * ntc - 1) / (threads * ntc));
             cudaError_t e = set_smem(k, smem);
             if (e != cudaSuccess) return e;

@@ -14,11 +14,12 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-secondary --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
 M=smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__inst_executed_pipe_fp64.sum,smsp__inst_executed_pipe_xu.sum,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum
 for m in sa case1 t2 mc c5; do timeout 400 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_$m.csv python tools/profile_kernels.py $m > gpurun_out/prof_$m.log 2>&1; done
-SABR_PRECISION=fp32 timeout 300 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_t2_fp32.csv python tools/profile_kernels.py t2 > /dev/null 2>&1
+for m in t2 c5 mc; do SABR_PRECISION=fp32 timeout 300 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_metrics_${m}_fp32.csv python tools/profile_kernels.py $m > gpurun_out/prof_${m}_fp32.log 2>&1; done
 if [ "${FULL:-1}" = "1" ]; then
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level -s 1 -c 1 -o gpurun_out/full_sa python tools/profile_kernels.py sa > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:sa_level -s 1 -c 1 -o gpurun_out/full_case1 python tools/profile_kernels.py case1 > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:mc_tile_kernel -s 2 -c 1 -o gpurun_out/full_t2 python tools/profile_kernels.py t2 > /dev/null 2>&1
+SABR_PRECISION=fp32 timeout 400 ncu --set full --clock-control none --import-source on -k regex:mc_tile_kernel -s 2 -c 1 -o gpurun_out/full_t2_fp32 python tools/profile_kernels.py t2 > /dev/null 2>&1
 fi
 # memory / race checks of the hot kernels (small shapes)
 timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python __graft_entry__.py smoke > gpurun_out/sanitizer_memcheck.log 2>&1

@@ -57,6 +57,8 @@ def main(mode):
     else:
         raise SystemExit(__doc__)
     print(mode, "evals" if hasattr(r, "evals") else "", getattr(r, "evals", r))
+    t = eng.last_timing()  # MC modes: candidate-path-steps of the run (tools/update_flops.py units)
+    print("path_steps", int(t.path_steps), "kernel_launches", int(t.kernel_launches))
     eng.close()
 
 

@@ -27,7 +27,7 @@ def per(path, prefix, units, pick=-1):
             None if xu is None else 32 * xu / units)
 
 
-def main(tag, copy=("sa", "case1", "t2", "t2_fp32", "mc", "c5")):
+def main(tag, copy=("sa", "case1", "t2", "t2_fp32", "mc", "mc_fp32", "c5", "c5_fp32")):
     src = os.path.join(ROOT, "gpurun_out")
     sa = per(os.path.join(src, "ncu_metrics_sa.csv"), ("sa_level_multi_kernel<0", "sa_level_kernel<0"), 1e7)
     c1 = per(os.path.join(src, "ncu_metrics_case1.csv"), ("sa_level_multi_kernel<1", "sa_level_kernel<1"), 1e7)
@@ -50,6 +50,33 @@ def main(tag, copy=("sa", "case1", "t2", "t2_fp32", "mc", "c5")):
         t2f = per(f32, "mc_tile_kernel_f32<8", 32 * 1e5 * 250)
         d["c4_fp32_xu_instr_per_candidate_path_step"] = t2f[6]
         d["c4_fp32_mc_kernel_ns"] = t2f[3]
+        d["c4_fp32_warp_instr_per_candidate_path_step"] = t2f[5]
+    c3 = os.path.join(src, "ncu_metrics_case1.csv")
+    if os.path.exists(c3):
+        d["c3_fp64_pipe_instr_per_eval"] = c1[4]
+        d["c3_warp_instr_per_eval"] = c1[5]
+    # C5 (one SA step of tools/profile_kernels.py c5: a single MC launch whose
+    # candidate-path-steps the tool prints) and single-candidate FP32 pricing
+    for name, csvf, prefix, log in (("c5", "ncu_metrics_c5.csv", "mc_tile_kernel<", "prof_c5.log"),
+                                    ("c5_fp32", "ncu_metrics_c5_fp32.csv", "mc_tile_kernel_f32<", "prof_c5_fp32.log")):
+        pc, pl = os.path.join(src, csvf), os.path.join(src, log)
+        if not (os.path.exists(pc) and os.path.exists(pl)):
+            continue
+        units = None
+        for line in open(pl):
+            if line.startswith("path_steps"):
+                units = float(line.split()[1])
+        if units:
+            r = per(pc, prefix, units)
+            if name == "c5":
+                d["c5_fp64_pipe_instr_per_candidate_path_step"] = r[4]
+                d["c5_flops_per_candidate_path_step"] = r[0]
+            else:
+                d["c5_fp32_xu_instr_per_candidate_path_step"] = r[6]
+    mf = os.path.join(src, "ncu_metrics_mc_fp32.csv")
+    if os.path.exists(mf):
+        r = per(mf, "mc_tile_kernel_f32<1", (1 << 20) * 124)
+        d["mc_single_fp32_xu_instr_per_path_step"] = r[6]
     with open(os.path.join(ROOT, "profiles", "fp64_per_eval.json"), "w") as f:
         json.dump(d, f, indent=1)
     for m in copy:
