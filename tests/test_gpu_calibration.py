@@ -150,3 +150,39 @@ def test_case2_formula_matches_reference(engine, ref, fx_surface):
     assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
     for k in r.params:
         assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("case", ["c4_shape", "c5_shape"])
+def test_case2_T2_candidate_block_invariance(engine, eq_surface, precision, case, monkeypatch):
+    """The MC tile kernels simulate CB candidates per thread (SABR_MC_CB: 1, 2,
+    4, 8, 16; the FP32 kernel runs them as packed FP32x2 pairs reading the
+    pair-interleaved coefficient rows, CB = 1 a half-idle pair on the plain
+    rows).  A candidate's arithmetic, its payoff column sums and the tile
+    reduction do not depend on CB, so the whole T_II report (evals, trace,
+    parameters, cost) must be bit-identical for every CB.  c4_shape: static
+    dynamics on one 250-step slice (the time-invariant-row kernels); c5_shape:
+    full Case II on the 20x30 synthetic surface (time-varying rows)."""
+    import bench
+
+    if case == "c4_shape":
+        surf = pkg.VolSurface(eq_surface.spot, [eq_surface.slices[2]])
+        fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
+        bounds = None
+        s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=3, workers=40, t_min=0.4, seed=5)
+        plan = pkg.SimulationPlan(num_paths=3000, seed=1, precision=precision)
+    else:
+        surf = pkg.parse_surface(os.path.join(os.path.dirname(__file__), "data", "synth20x30.csv"))
+        fixed, bounds = None, bench.c5_bounds()
+        s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=24, t_min=0.9, seed=4)
+        plan = pkg.SimulationPlan(num_paths=300, seed=2, precision=precision)
+    reps = {}
+    for cb in (1, 2, 4, 8, 16):
+        monkeypatch.setenv("SABR_MC_CB", str(cb))
+        reps[cb] = engine.calibrate_case2_T2(surf, bounds, s, plan, fixed)
+    a = reps[8]
+    for cb, b in reps.items():
+        assert b.evals == a.evals, cb
+        assert b.final_cost == a.final_cost, (cb, b.final_cost, a.final_cost)
+        assert b.params == a.params, cb
+        assert b.temperature_trace == a.temperature_trace, cb
