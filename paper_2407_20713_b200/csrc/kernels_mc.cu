@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
                     // beta == 1 (mc.cpp:99-100: nu_hat = alpha): bm1 = 0 exactly,
                     // so the fma returns la exactly for any finite x - no select
                     const double arg = fma(bm1[cc], lnf0 + x[cc], la[cc]);
-                    const double nh = exp_tab<kExpRep>(arg, tab_lane);
+                    const double nh = exp_mc<kExpRep>(arg, tab_lane);
                     la[cc] += fma(qa[cc].x, z1, -qa[cc].y);
                     const double u = fma(qb[cc].y, z2, qb[cc].x * z1);
                     x[cc] = fma(nh, fma(-nh, h, u), x[cc]);
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kMcThreads) mc_cliquet_kernel(const __grid_con
                 double z1, z2;
                 box_muller_tab(ua, ub, ltab, sctab, z1, z2);
                 const StepCoef q = P.coef[sl.step_off + i];
-                const double nh = exp_tab(logn ? la : fma(bm1, sl.lnf0 + x, la), tab);
+                const double nh = exp_mc(logn ? la : fma(bm1, sl.lnf0 + x, la), tab);
                 la += fma(q.c1, z1, -q.c2);
                 const double u = fma(q.ss, z2, q.rs * z1);
                 x = fma(nh, fma(-nh, __ldg(P.hdt + sl.step_off + i), u), x);

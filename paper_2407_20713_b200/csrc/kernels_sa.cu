@@ -985,15 +985,22 @@ constexpr int kPairMinCtas = 11;
 // threads per CTA and CTAs per SM (launch bound) of the C-chain level kernel:
 // C = 1, 2 cover kLevelThreads chains per CTA; C = 3 (SABR_SA_CPT=3, A/B)
 // uses one warp of 96 chains and 8 CTAs per SM (<= 255 registers)
-// Case I with two chains per thread (r02): two-warp CTAs of 128 chains, 6 per
-// SM at 168 registers, so each CTA has room for the 8-copy bank-replicated exp
-// table (16 KB; 11 one-warp CTAs per SM could not hold it) and its 8 exp
-// lookups per eval stop conflicting (ncu r02d: 14.9M excess shared wavefronts
-// per level with one copy)
+// kCase1Rep (A/B, off): Case I with two chains per thread in two-warp CTAs of
+// 128 chains, 6 per SM at 168 registers, which leaves each CTA room for the
+// 8-copy bank-replicated exp table (11 one-warp CTAs per SM cannot hold it).
+// Its 8 exp lookups per eval then stop conflicting (ncu: 14.9M -> 0.08M excess
+// shared wavefronts per level), but the kernel is bound by FP64 dependency
+// latency and C3 ran 1.3% slower (1.867e10 -> 1.843e10 evals/s), so the
+// one-warp CTAs with one table copy stay.
+constexpr bool kCase1Rep = false;
 template <int KIND, int C>
-constexpr int level_nt() { return C == 3 ? 32 : (KIND == OBJ_CASE1 && C == 2) ? 64 : kLevelThreads / C; }
+constexpr int level_nt() {
+    return C == 3 ? 32 : (kCase1Rep && KIND == OBJ_CASE1 && C == 2) ? 64 : kLevelThreads / C;
+}
 template <int KIND, int C>
-constexpr int level_min_ctas() { return C == 3 ? 8 : (KIND == OBJ_CASE1 && C == 2) ? 6 : kPairMinCtas; }
+constexpr int level_min_ctas() {
+    return C == 3 ? 8 : (kCase1Rep && KIND == OBJ_CASE1 && C == 2) ? 6 : kPairMinCtas;
+}
 // copies of the bank-replicated exp table (device_common.cuh: kExpRep) per
 // objective in the C-chain level kernel
 template <int KIND>
@@ -1196,9 +1203,9 @@ __global__ void __launch_bounds__(level_nt<KIND, C>(), level_min_ctas<KIND, C>()
     sa_level_multi_kernel(const __grid_constant__ SurfaceView sv, const __grid_constant__ SaLevelArgs a,
                           const int64_t level, const double temp, const double inv_temp) {
     constexpr int NT = level_nt<KIND, C>();
-    // the static objective's pow and the Case I closed forms' exp read the
-    // bank-replicated exp table (Case I: two-warp CTAs, level_nt)
-    constexpr bool kRep = GK == kGridQR && (KIND == OBJ_STATIC || (KIND == OBJ_CASE1 && C == 2));
+    // the static objective's pow reads the bank-replicated exp table (Case I:
+    // one copy, kCase1Rep)
+    constexpr bool kRep = GK == kGridQR && (KIND == OBJ_STATIC || (kCase1Rep && KIND == OBJ_CASE1 && C == 2));
     constexpr int kRepN = rep_copies<KIND>();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ RedShared<NT> rs;
