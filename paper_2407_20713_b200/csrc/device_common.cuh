@@ -784,11 +784,15 @@ __device__ __forceinline__ void case1_closed_pair(double x, const double2* __res
     }
 }
 
-// case1_closed_pair with 1/x supplied (ix, within a few ulp of the quotient):
-// the scale factors 6/x^3, 2/x^2 and 3/x^4 from it, the brackets unchanged
+// case1_closed_pair with its scale factors supplied (sa, sb within a few ulp
+// of the quotients): PAIR 0 takes sa = 6/x^3 for both functionals, PAIR 1
+// sa = 2/x^2 and sb = 3/x^4.  The brackets are the reference's
+// (analytics.cpp:46-67) operation for operation; where one of its products is
+// exact (x*x/2, 2*(e-1), 8*e, 2*x*(x-3) = 2*RN(x*(x-3))) the product and the
+// following sum are one FMA, which rounds once, as the reference's sum does.
 template <int PAIR, int STRIDE = 1>
-__device__ __forceinline__ void case1_closed_pair_r(double x, double ix, const double2* __restrict__ tab,
-                                                    double& f, double& g) {
+__device__ __forceinline__ void case1_closed_pair_r(double x, double sa, double sb,
+                                                    const double2* __restrict__ tab, double& f, double& g) {
     // exp(-x) for x >= 0.25 (never NaN: x = 2bT or (a+b)T from the box);
     // past x = 700 the clamp's e ~ 1e-304 leaves every bracket the double it
     // is with e = 0 (each bracket holds a term >= x - 1), so exp_tab's
@@ -796,15 +800,16 @@ __device__ __forceinline__ void case1_closed_pair_r(double x, double ix, const d
     const double e = exp_tab_unsat<STRIDE>(fmax(-x, -700.0), tab);
     if constexpr (PAIR == 0) {
         const double x2 = SABR_MUL(x, x);
-        const double c6 = (6.0 * ix) * (ix * ix);
-        f = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), x), 1.0), e));
-        g = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(x, SABR_ADD(e, 1.0))));
+        // x*x/2 - x + 1 - e
+        f = SABR_MUL(sa, SABR_SUB(SABR_ADD(fma(x2, 0.5, -x), 1.0), e));
+        // 2*(e-1) + x*(e+1)
+        g = SABR_MUL(sa, fma(2.0, SABR_SUB(e, 1.0), SABR_MUL(x, SABR_ADD(e, 1.0))));
     } else {
-        const double r2 = ix * ix;
-        f = SABR_MUL(2.0 * r2, SABR_SUB(e, SABR_SUB(1.0, x)));
-        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
-                                     SABR_MUL(SABR_MUL(2.0, x), SABR_SUB(x, 3.0)));
-        g = SABR_MUL(3.0 * (r2 * r2), poly);
+        // e - (1 - x)
+        f = SABR_MUL(sa, SABR_SUB(e, SABR_SUB(1.0, x)));
+        // e*e - 8*e + 7 + 2*x*(x-3)
+        const double poly = fma(2.0, SABR_MUL(x, SABR_SUB(x, 3.0)), SABR_ADD(fma(-8.0, e, SABR_MUL(e, e)), 7.0));
+        g = SABR_MUL(sb, poly);
     }
 }
 
@@ -812,11 +817,11 @@ __device__ __forceinline__ void case1_closed_pair_r(double x, double ix, const d
 // same branch (the rule late in a schedule, when the chains cluster), their
 // evaluations share one branch body and interleave (C-fold ILP); mixed
 // threads evaluate chain by chain.  Per-chain results do not depend on C.
-// RCP: the closed forms take 1/x from ix (case1_closed_pair_r)
+// RCP: the closed forms take their scale factors from sa, sb (case1_closed_pair_r)
 template <int PAIR, int C, int STRIDE = 1, bool RCP = false>
 __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
                                              const double2* __restrict__ tab, double (&f)[C], double (&g)[C],
-                                             const double (&ix)[C]) {
+                                             const double (&sa)[C], const double (&sb)[C]) {
     constexpr double kXSwitch = 0.25;  // analytics.cpp:21
     bool all_series = true, all_closed = true;
 #pragma unroll
@@ -830,14 +835,14 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
     } else if (all_closed) {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], ix[c], tab, f[c], g[c]);
+            if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
             else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
         }
     } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (x[c] < kXSwitch) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
-            else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], ix[c], tab, f[c], g[c]);
+            else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
             else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
         }
     }
@@ -848,21 +853,22 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
 // reference's quotients; they scale the cancelling brackets, they are not
 // inside them) and exp by table (exp_tab, ~0.5 ulp).  The brackets keep the
 // reference's operation order and roundings.
-// ixb, ixab: 1/(2bT) and 1/((a+b)T) as 1/(2b) * 1/T, 1/(a+b) * 1/T (the
-// scale factors of the closed forms, case1_closed_pair_r).
+// The closed forms' scale factors as per-vector constants times per-slice
+// powers of 1/T (case1_scales): sb0 = 6/(2bT)^3, sa1 = 2/((a+b)T)^2,
+// sb1 = 3/((a+b)T)^4.
 __device__ __forceinline__ void dyn_coeffs_case1_fast(double rho0, double nu0, double a, double b, double T,
-                                                      double ixb, double ixab,
+                                                      double s6, double s2, double s3,
                                                       const double* __restrict__ ser,
                                                       const double2* __restrict__ tab, double& nu1_sq,
                                                       double& nu2_sq, double& eta1, double& eta2_sq) {
     const double xb[1] = {SABR_MUL(SABR_MUL(2.0, b), T)};
     const double xab[1] = {SABR_MUL(SABR_ADD(a, b), T)};
-    const double rb[1] = {ixb}, rab[1] = {ixab};
+    const double sa0[1] = {s6}, sa1[1] = {s2}, sb1[1] = {s3};
     const double nn = SABR_MUL(nu0, nu0);
     const double nr = SABR_MUL(nu0, rho0);
     double f1[1], f2[1], g1[1], g2[1];
-    case1_pair_n<0, 1, 1, true>(xb, ser, tab, f1, f2, rb);
-    case1_pair_n<1, 1, 1, true>(xab, ser, tab, g1, g2, rab);
+    case1_pair_n<0, 1, 1, true>(xb, ser, tab, f1, f2, sa0, sa0);
+    case1_pair_n<1, 1, 1, true>(xab, ser, tab, g1, g2, sa1, sb1);
     nu1_sq = SABR_MUL(nn, f1[0]);
     nu2_sq = SABR_MUL(nn, f2[0]);
     eta1 = SABR_MUL(nr, g1[0]);

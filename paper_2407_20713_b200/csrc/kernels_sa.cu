@@ -387,11 +387,12 @@ struct QGrid {
     const double* R;    // [ns][kQrStride], 16-byte aligned
     const double* ser;  // [4][kSeriesStride] Case I series tables (horner_s)
     const double2* tab;
-    const double* iT;   // [ns] 1 / T (Case I: the closed forms' 1/x = 1/(2b) * 1/T)
+    const double* iT;   // [4][ns] 1/T^2, 1/T^3, 1/T^4 and 1/T (Case I: the closed forms'
+                        // scale factors 6/(2bT)^3 = 6/(2b)^3 * 1/T^3, ..., case1_cost_n)
 };
 
 __host__ __device__ inline size_t qstage_bytes(int ns) {
-    return sizeof(double) * (4 * kSeriesStride + static_cast<size_t>(kQrStride + 4) * ns);
+    return sizeof(double) * (4 * kSeriesStride + static_cast<size_t>(kQrStride + 7) * ns);
 }
 
 __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
@@ -405,7 +406,11 @@ __device__ QGrid stage_qgrid(const SurfaceView& sv, unsigned char* smem) {
         d[i] = sv.T[i];
         d[ns + i] = sv.lnf_hi[i];
         d[2 * ns + i] = sv.lnf_lo[i];
-        d[3 * ns + i] = 1.0 / sv.T[i];
+        const double it = 1.0 / sv.T[i], it2 = it * it;
+        d[3 * ns + i] = it2;
+        d[4 * ns + i] = it2 * it;
+        d[5 * ns + i] = it2 * it2;
+        d[6 * ns + i] = it;
     }
     __syncthreads();
     QGrid g;
@@ -449,16 +454,30 @@ __device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
     return qr_cost(static_qterms(v, pw, g.T[0]), load_qr(g.R));
 }
 
+// Per-vector constants of the Case I closed forms' scale factors (r02):
+// 6/(2b)^3, 2/(a+b)^2 and 3/(a+b)^4, times the CTA's 1/T^3, 1/T^2, 1/T^4 per
+// slice give 6/x^3 (x = 2bT), 2/x^2 and 3/x^4 (x = (a+b)T) within a few ulp.
+// Only the closed-form branch (x >= 0.25, so b > 0 and a + b > 0) uses them.
+__device__ __forceinline__ void case1_scales(double a, double b, double& k6, double& k2, double& k3) {
+    const double rb = fast_rcp(SABR_MUL(2.0, b)), rab = fast_rcp(SABR_ADD(a, b));
+    const double rab2 = rab * rab;
+    k6 = (6.0 * rb) * (rb * rb);
+    k2 = 2.0 * rab2;
+    k3 = 3.0 * (rab2 * rab2);
+}
+
 // The Case I objective of one vector (case1_cost_n's arithmetic, bit for bit).
 __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
     double sum = 0.0;
     const double omb = 1.0 - v[1];
-    const double rb = fast_rcp(SABR_MUL(2.0, v[5])), rab = fast_rcp(SABR_ADD(v[4], v[5]));
+    double k6, k2, k3;
+    case1_scales(v[4], v[5], k6, k2, k3);
     const double ia = fast_rcp(v[0]);
     for (int i = 0; i < g.ns; ++i) {
-        const double T = g.T[i], iT = g.iT[i];
+        const double T = g.T[i];
         double n1, n2, e1, e2;
-        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, rb * iT, rab * iT, g.ser, g.tab, n1, n2, e1, e2);
+        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, k6 * g.iT[g.ns + i], k2 * g.iT[i], k3 * g.iT[2 * g.ns + i],
+                              g.ser, g.tab, n1, n2, e1, e2);
         const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
         QuadTerms t;
         dynamic_quad_terms_r(n1, n2, e1, e2, v[1], v[0] * fast_rcp(pw), pw * ia, T, t.c0, t.a1, t.a2);
@@ -507,15 +526,14 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
     // rcp(f^(1-beta)) per slice.  Each factor is within a few ulp of the
     // per-slice quotient; it scales a cancelling bracket, it is not inside
     // one (the brackets keep the reference's operations, analytics.cpp:47-67).
-    // per chain, slice-independent: 2b, a+b, their reciprocals, rcp(alpha),
-    // nu0^2, nu0 rho0, (nu0 rho0)^2
-    double b2[C], ab[C], rb[C], rab[C], ia[C], nn[C], nr[C], nr2[C];
+    // per chain, slice-independent: 2b, a+b, the scale-factor constants
+    // (case1_scales), rcp(alpha), nu0^2, nu0 rho0, (nu0 rho0)^2
+    double b2[C], ab[C], k6[C], k2[C], k3[C], ia[C], nn[C], nr[C], nr2[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         b2[c] = SABR_MUL(2.0, v[c][5]);
         ab[c] = SABR_ADD(v[c][4], v[c][5]);
-        rb[c] = fast_rcp(b2[c]);
-        rab[c] = fast_rcp(ab[c]);
+        case1_scales(v[c][4], v[c][5], k6[c], k2[c], k3[c]);
         ia[c] = fast_rcp(v[c][0]);
         nn[c] = SABR_MUL(v[c][3], v[c][3]);
         nr[c] = SABR_MUL(v[c][3], v[c][2]);
@@ -524,16 +542,17 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
 #pragma unroll
     for (int c = 0; c < C; ++c) out[c] = 0.0;
     for (int i = 0; i < g.ns; ++i) {
-        const double T = g.T[i], iT = g.iT[i];
+        const double T = g.T[i], iT2 = g.iT[i], iT3 = g.iT[g.ns + i], iT4 = g.iT[2 * g.ns + i];
         const QrFactor f = load_qr(g.R + kQrStride * i);
         // dyn_coeffs_case1_fast for the C chains, branch bodies shared
-        double xb[C], xab[C], ixb[C], ixab[C], f1[C], f2[C], g1[C], g2[C];
+        double xb[C], xab[C], s6[C], s2[C], s3[C], f1[C], f2[C], g1[C], g2[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             xb[c] = SABR_MUL(b2[c], T);
             xab[c] = SABR_MUL(ab[c], T);
-            ixb[c] = rb[c] * iT;
-            ixab[c] = rab[c] * iT;
+            s6[c] = k6[c] * iT3;
+            s2[c] = k2[c] * iT2;
+            s3[c] = k3[c] * iT4;
         }
         // both functional pairs of every chain in the closed-form regime (the
         // rule on C3's surfaces): one straight-line block, 2C independent
@@ -544,12 +563,12 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
         if (all_closed) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                case1_closed_pair_r<0, STRIDE>(xb[c], ixb[c], tab, f1[c], f2[c]);
-                case1_closed_pair_r<1, STRIDE>(xab[c], ixab[c], tab, g1[c], g2[c]);
+                case1_closed_pair_r<0, STRIDE>(xb[c], s6[c], s6[c], tab, f1[c], f2[c]);
+                case1_closed_pair_r<1, STRIDE>(xab[c], s2[c], s3[c], tab, g1[c], g2[c]);
             }
         } else {
-            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, ixb);
-            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, ixab);
+            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, s6, s6);
+            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, s2, s3);
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
