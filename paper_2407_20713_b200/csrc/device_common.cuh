@@ -697,29 +697,39 @@ SABR_HD void dynamic_quad_terms(double nu1_sq, double nu2_sq, double eta1, doubl
     c0 = fma(inv, B * T, inv);
 }
 
-// dynamic_quad_terms with 1/omega and omega supplied (beta fixed: alpha times
-// the CTA's 1 / f^(1-beta), f^(1-beta) times 1/alpha)
-SABR_HD void dynamic_quad_terms_r(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double beta,
-                                  double inv, double omega, double T, double& c0, double& a1, double& a2) {
+// The Case I terms of the factored cost (dynamic_quad_terms) written on the
+// scaled functionals of a slice (r02),
+//     Af1 = nu0^2/6 f_nu1,  Ef2 = nu0^2/12 f_nu2,  dg1 = nu0 rho0/4 f_eta1 = eta1/4,
+//     bg2 = (nu0 rho0)^2/8 f_eta2 = eta2^2/8,
+// so that with q = (1-beta)/omega
+//     A1/omega = 2 dg1 - q/2
+//     A2/omega = k/24 omega - dg1 + q (1/4 + (1-beta)/12),  k/24 = Af1 + bg2 - 6 dg1^2
+//     B        = q^2/24 + beta dg1 / omega + Ef2 - bg2
+//     C0       = 1/omega + (1/omega) B T.
+// The closed forms produce the scaled functionals directly: each chain's
+// constant (nu0^2/6, ...) is folded into its scale factor (case1_scales), so
+// the slice costs no separate multiplications by nu0, rho0 and 1/24.  Each term
+// is within a few ulp of the reference's (dynamic_implied_vol,
+// analytics.cpp:291-312); every Case I path uses these functions, so the
+// kernel variants agree bit for bit, and with beta = 1 (q = 0 exactly) the
+// general form reduces term by term to dynamic_quad_terms_b1.
+SABR_HD void dynamic_quad_terms_k(double Af1, double Ef2, double dg1, double bg2, double beta, double inv,
+                                  double omega, double T, double& c0, double& a1, double& a2) {
     const double omb = 1.0 - beta;
     const double q = omb * inv;
-    const double p = q - eta1;
-    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
-    a1 = -0.5 * p;
-    a2 = fma(k * (1.0 / 24.0), omega, fma(0.25, p, (omb * q) * (1.0 / 12.0)));
-    const double B = fma(q * (1.0 / 24.0), q, fma((0.25 * beta) * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0)));
+    const double k24 = fma(-6.0 * dg1, dg1, Af1 + bg2);
+    a1 = fma(-0.5, q, dg1 + dg1);
+    a2 = fma(k24, omega, fma(q, fma(omb, 1.0 / 12.0, 0.25), -dg1));
+    const double B = fma(beta * dg1, inv, fma(q * (1.0 / 24.0), q, Ef2 - bg2));
     c0 = fma(inv, B * T, inv);
 }
-
-// dynamic_quad_terms_r at beta = 1 (f^(1-beta) = 1: 1/omega = alpha, omega =
-// rcp(alpha)): with 1 - beta = 0, q = 0 and p = -eta1, the same roundings as
-// the general form term by term (each dropped operand is an exact zero)
-SABR_HD void dynamic_quad_terms_b1(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double inv,
-                                   double omega, double T, double& c0, double& a1, double& a2) {
-    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
-    a1 = 0.5 * eta1;
-    a2 = fma(k * (1.0 / 24.0), omega, -0.25 * eta1);
-    const double B = fma(0.25 * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0));
+// beta = 1: 1/omega = alpha, omega = rcp(alpha), q = 0
+SABR_HD void dynamic_quad_terms_b1(double Af1, double Ef2, double dg1, double bg2, double inv, double omega,
+                                   double T, double& c0, double& a1, double& a2) {
+    const double k24 = fma(-6.0 * dg1, dg1, Af1 + bg2);
+    a1 = dg1 + dg1;
+    a2 = fma(k24, omega, -dg1);
+    const double B = fma(dg1, inv, Ef2 - bg2);
     c0 = fma(inv, B * T, inv);
 }
 
@@ -785,8 +795,9 @@ __device__ __forceinline__ void case1_closed_pair(double x, const double2* __res
 }
 
 // case1_closed_pair with its scale factors supplied (sa, sb within a few ulp
-// of the quotients): PAIR 0 takes sa = 6/x^3 for both functionals, PAIR 1
-// sa = 2/x^2 and sb = 3/x^4.  The brackets are the reference's
+// of the quotients times the chain's constants, case1_scales): PAIR 0 takes
+// sa ~ nu0^2 / x^3 and sb ~ nu0^2 / (2 x^3), PAIR 1 sa ~ nu0 rho0 / (2 x^2) and
+// sb ~ 3 (nu0 rho0)^2 / (8 x^4).  The brackets are the reference's
 // (analytics.cpp:46-67) operation for operation; where one of its products is
 // exact (x*x/2, 2*(e-1), 8*e, 2*x*(x-3) = 2*RN(x*(x-3))) the product and the
 // following sum are one FMA, which rounds once, as the reference's sum does.
@@ -803,7 +814,7 @@ __device__ __forceinline__ void case1_closed_pair_r(double x, double sa, double 
         // x*x/2 - x + 1 - e
         f = SABR_MUL(sa, SABR_SUB(SABR_ADD(fma(x2, 0.5, -x), 1.0), e));
         // 2*(e-1) + x*(e+1)
-        g = SABR_MUL(sa, fma(2.0, SABR_SUB(e, 1.0), SABR_MUL(x, SABR_ADD(e, 1.0))));
+        g = SABR_MUL(sb, fma(2.0, SABR_SUB(e, 1.0), SABR_MUL(x, SABR_ADD(e, 1.0))));
     } else {
         // e - (1 - x)
         f = SABR_MUL(sa, SABR_SUB(e, SABR_SUB(1.0, x)));
@@ -818,10 +829,12 @@ __device__ __forceinline__ void case1_closed_pair_r(double x, double sa, double 
 // evaluations share one branch body and interleave (C-fold ILP); mixed
 // threads evaluate chain by chain.  Per-chain results do not depend on C.
 // RCP: the closed forms take their scale factors from sa, sb (case1_closed_pair_r)
+// (the series values times ca, cb: the chain's constants of case1_scales)
 template <int PAIR, int C, int STRIDE = 1, bool RCP = false>
 __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
                                              const double2* __restrict__ tab, double (&f)[C], double (&g)[C],
-                                             const double (&sa)[C], const double (&sb)[C]) {
+                                             const double (&sa)[C], const double (&sb)[C],
+                                             const double (&ca)[C], const double (&cb)[C]) {
     constexpr double kXSwitch = 0.25;  // analytics.cpp:21
     bool all_series = true, all_closed = true;
 #pragma unroll
@@ -831,7 +844,13 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
     }
     if (all_series) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+        for (int c = 0; c < C; ++c) {
+            case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+            if constexpr (RCP) {
+                f[c] *= ca[c];
+                g[c] *= cb[c];
+            }
+        }
     } else if (all_closed) {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
@@ -841,8 +860,13 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
     } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            if (x[c] < kXSwitch) case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
-            else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
+            if (x[c] < kXSwitch) {
+                case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
+                if constexpr (RCP) {
+                    f[c] *= ca[c];
+                    g[c] *= cb[c];
+                }
+            } else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
             else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
         }
     }
@@ -853,26 +877,24 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
 // reference's quotients; they scale the cancelling brackets, they are not
 // inside them) and exp by table (exp_tab, ~0.5 ulp).  The brackets keep the
 // reference's operation order and roundings.
-// The closed forms' scale factors as per-vector constants times per-slice
-// powers of 1/T (case1_scales): sb0 = 6/(2bT)^3, sa1 = 2/((a+b)T)^2,
-// sb1 = 3/((a+b)T)^4.
-__device__ __forceinline__ void dyn_coeffs_case1_fast(double rho0, double nu0, double a, double b, double T,
-                                                      double s6, double s2, double s3,
-                                                      const double* __restrict__ ser,
-                                                      const double2* __restrict__ tab, double& nu1_sq,
-                                                      double& nu2_sq, double& eta1, double& eta2_sq) {
+// One vector's four scaled functionals of a slice (dynamic_quad_terms_k):
+// sc = the per-slice scale factors and cs = the chain constants of
+// case1_scales.
+__device__ __forceinline__ void case1_functionals(double a, double b, double T, const double (&sc)[4],
+                                                  const double (&cs)[4], const double* __restrict__ ser,
+                                                  const double2* __restrict__ tab, double& Af1, double& Ef2,
+                                                  double& dg1, double& bg2) {
     const double xb[1] = {SABR_MUL(SABR_MUL(2.0, b), T)};
     const double xab[1] = {SABR_MUL(SABR_ADD(a, b), T)};
-    const double sa0[1] = {s6}, sa1[1] = {s2}, sb1[1] = {s3};
-    const double nn = SABR_MUL(nu0, nu0);
-    const double nr = SABR_MUL(nu0, rho0);
-    double f1[1], f2[1], g1[1], g2[1];
-    case1_pair_n<0, 1, 1, true>(xb, ser, tab, f1, f2, sa0, sa0);
-    case1_pair_n<1, 1, 1, true>(xab, ser, tab, g1, g2, sa1, sb1);
-    nu1_sq = SABR_MUL(nn, f1[0]);
-    nu2_sq = SABR_MUL(nn, f2[0]);
-    eta1 = SABR_MUL(nr, g1[0]);
-    eta2_sq = SABR_MUL(SABR_MUL(nr, nr), g2[0]);
+    const double s0[1] = {sc[0]}, s1[1] = {sc[1]}, s2[1] = {sc[2]}, s3[1] = {sc[3]};
+    const double c0[1] = {cs[0]}, c1[1] = {cs[1]}, c2[1] = {cs[2]}, c3[1] = {cs[3]};
+    double F1[1], F2[1], G1[1], G2[1];
+    case1_pair_n<0, 1, 1, true>(xb, ser, tab, F1, F2, s0, s1, c0, c1);
+    case1_pair_n<1, 1, 1, true>(xab, ser, tab, G1, G2, s2, s3, c2, c3);
+    Af1 = F1[0];
+    Ef2 = F2[0];
+    dg1 = G1[0];
+    bg2 = G2[0];
 }
 #endif
 

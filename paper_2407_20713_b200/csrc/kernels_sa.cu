@@ -454,33 +454,53 @@ __device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
     return qr_cost(static_qterms(v, pw, g.T[0]), load_qr(g.R));
 }
 
-// Per-vector constants of the Case I closed forms' scale factors (r02):
-// 6/(2b)^3, 2/(a+b)^2 and 3/(a+b)^4, times the CTA's 1/T^3, 1/T^2, 1/T^4 per
-// slice give 6/x^3 (x = 2bT), 2/x^2 and 3/x^4 (x = (a+b)T) within a few ulp.
-// Only the closed-form branch (x >= 0.25, so b > 0 and a + b > 0) uses them.
-__device__ __forceinline__ void case1_scales(double a, double b, double& k6, double& k2, double& k3) {
+// Per-vector constants of the Case I closed forms' scale factors (r02): with
+// the CTA's 1/T^3, 1/T^2, 1/T^4 per slice, P1/T^3 = nu0^2/6 * 6/x^3 (x = 2bT),
+// Q1/T^2 = nu0 rho0/4 * 2/x^2 and Q2/T^4 = (nu0 rho0)^2/8 * 3/x^4 (x = (a+b)T)
+// within a few ulp: the closed forms then yield the scaled functionals of
+// dynamic_quad_terms_k.  Only the closed-form branch (x >= 0.25, so b > 0 and
+// a + b > 0) uses them.
+__device__ __forceinline__ void case1_scales(double nu0, double rho0, double a, double b, double& P1, double& Q1,
+                                             double& Q2) {
     const double rb = fast_rcp(SABR_MUL(2.0, b)), rab = fast_rcp(SABR_ADD(a, b));
-    const double rab2 = rab * rab;
-    k6 = (6.0 * rb) * (rb * rb);
-    k2 = 2.0 * rab2;
-    k3 = 3.0 * (rab2 * rab2);
+    const double nr = nu0 * rho0, rab2 = rab * rab;
+    P1 = (nu0 * nu0) * (rb * (rb * rb));
+    Q1 = (0.5 * nr) * rab2;
+    Q2 = (0.375 * (nr * nr)) * (rab2 * rab2);
+}
+// the series branch's constants: nu0^2/6, nu0^2/12, nu0 rho0/4, (nu0 rho0)^2/8
+__device__ __forceinline__ void case1_series_consts(double nu0, double rho0, double (&c)[4]) {
+    const double nn = nu0 * nu0, nr = nu0 * rho0;
+    c[0] = nn * (1.0 / 6.0);
+    c[1] = 0.5 * c[0];
+    c[2] = 0.25 * nr;
+    c[3] = 0.125 * (nr * nr);
+}
+// the four scale factors of slice i (g.iT: 1/T^2, 1/T^3, 1/T^4 blocks)
+__device__ __forceinline__ void case1_slice_scales(double P1, double Q1, double Q2, double iT2, double iT3,
+                                                   double iT4, double (&sc)[4]) {
+    sc[0] = P1 * iT3;
+    sc[1] = 0.5 * sc[0];
+    sc[2] = Q1 * iT2;
+    sc[3] = Q2 * iT4;
 }
 
 // The Case I objective of one vector (case1_cost_n's arithmetic, bit for bit).
 __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
     double sum = 0.0;
     const double omb = 1.0 - v[1];
-    double k6, k2, k3;
-    case1_scales(v[4], v[5], k6, k2, k3);
+    double P1, Q1, Q2, cs[4];
+    case1_scales(v[3], v[2], v[4], v[5], P1, Q1, Q2);
+    case1_series_consts(v[3], v[2], cs);
     const double ia = fast_rcp(v[0]);
     for (int i = 0; i < g.ns; ++i) {
         const double T = g.T[i];
-        double n1, n2, e1, e2;
-        dyn_coeffs_case1_fast(v[2], v[3], v[4], v[5], T, k6 * g.iT[g.ns + i], k2 * g.iT[i], k3 * g.iT[2 * g.ns + i],
-                              g.ser, g.tab, n1, n2, e1, e2);
+        double sc[4], Af1, Ef2, dg1, bg2;
+        case1_slice_scales(P1, Q1, Q2, g.iT[i], g.iT[g.ns + i], g.iT[2 * g.ns + i], sc);
+        case1_functionals(v[4], v[5], T, sc, cs, g.ser, g.tab, Af1, Ef2, dg1, bg2);
         const double pw = pow_fwd(omb, g.lnf_hi[i], g.lnf_lo[i], g.tab);
         QuadTerms t;
-        dynamic_quad_terms_r(n1, n2, e1, e2, v[1], v[0] * fast_rcp(pw), pw * ia, T, t.c0, t.a1, t.a2);
+        dynamic_quad_terms_k(Af1, Ef2, dg1, bg2, v[1], v[0] * fast_rcp(pw), pw * ia, T, t.c0, t.a1, t.a2);
         sum += qr_cost(t, load_qr(g.R + kQrStride * i));
     }
     return sum;
@@ -527,17 +547,14 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
     // per-slice quotient; it scales a cancelling bracket, it is not inside
     // one (the brackets keep the reference's operations, analytics.cpp:47-67).
     // per chain, slice-independent: 2b, a+b, the scale-factor constants
-    // (case1_scales), rcp(alpha), nu0^2, nu0 rho0, (nu0 rho0)^2
-    double b2[C], ab[C], k6[C], k2[C], k3[C], ia[C], nn[C], nr[C], nr2[C];
+    // (case1_scales) and rcp(alpha)
+    double b2[C], ab[C], P1[C], Q1[C], Q2[C], ia[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         b2[c] = SABR_MUL(2.0, v[c][5]);
         ab[c] = SABR_ADD(v[c][4], v[c][5]);
-        case1_scales(v[c][4], v[c][5], k6[c], k2[c], k3[c]);
+        case1_scales(v[c][3], v[c][2], v[c][4], v[c][5], P1[c], Q1[c], Q2[c]);
         ia[c] = fast_rcp(v[c][0]);
-        nn[c] = SABR_MUL(v[c][3], v[c][3]);
-        nr[c] = SABR_MUL(v[c][3], v[c][2]);
-        nr2[c] = SABR_MUL(nr[c], nr[c]);
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) out[c] = 0.0;
@@ -545,14 +562,17 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
         const double T = g.T[i], iT2 = g.iT[i], iT3 = g.iT[g.ns + i], iT4 = g.iT[2 * g.ns + i];
         const QrFactor f = load_qr(g.R + kQrStride * i);
         // dyn_coeffs_case1_fast for the C chains, branch bodies shared
-        double xb[C], xab[C], s6[C], s2[C], s3[C], f1[C], f2[C], g1[C], g2[C];
+        double xb[C], xab[C], sa0[C], sb0[C], sa1[C], sb1[C], f1[C], f2[C], g1[C], g2[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             xb[c] = SABR_MUL(b2[c], T);
             xab[c] = SABR_MUL(ab[c], T);
-            s6[c] = k6[c] * iT3;
-            s2[c] = k2[c] * iT2;
-            s3[c] = k3[c] * iT4;
+            double sc[4];
+            case1_slice_scales(P1[c], Q1[c], Q2[c], iT2, iT3, iT4, sc);
+            sa0[c] = sc[0];
+            sb0[c] = sc[1];
+            sa1[c] = sc[2];
+            sb1[c] = sc[3];
         }
         // both functional pairs of every chain in the closed-form regime (the
         // rule on C3's surfaces): one straight-line block, 2C independent
@@ -563,20 +583,28 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
         if (all_closed) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                case1_closed_pair_r<0, STRIDE>(xb[c], s6[c], s6[c], tab, f1[c], f2[c]);
-                case1_closed_pair_r<1, STRIDE>(xab[c], s2[c], s3[c], tab, g1[c], g2[c]);
+                case1_closed_pair_r<0, STRIDE>(xb[c], sa0[c], sb0[c], tab, f1[c], f2[c]);
+                case1_closed_pair_r<1, STRIDE>(xab[c], sa1[c], sb1[c], tab, g1[c], g2[c]);
             }
         } else {
-            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, s6, s6);
-            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, s2, s3);
+            double ca0[C], cb0[C], ca1[C], cb1[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                double cs[4];
+                case1_series_consts(v[c][3], v[c][2], cs);
+                ca0[c] = cs[0];
+                cb0[c] = cs[1];
+                ca1[c] = cs[2];
+                cb1[c] = cs[3];
+            }
+            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, sa0, sb0, ca0, cb0);
+            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, sa1, sb1, ca1, cb1);
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             QuadTerms t;
-            const double n1 = SABR_MUL(nn[c], f1[c]), n2 = SABR_MUL(nn[c], f2[c]);
-            const double e1 = SABR_MUL(nr[c], g1[c]), e2 = SABR_MUL(nr2[c], g2[c]);
             if constexpr (BETA1) {
-                dynamic_quad_terms_b1(n1, n2, e1, e2, v[c][0], ia[c], T, t.c0, t.a1, t.a2);
+                dynamic_quad_terms_b1(f1[c], f2[c], g1[c], g2[c], v[c][0], ia[c], T, t.c0, t.a1, t.a2);
             } else {
                 double pw, ipw;
                 if (pw_fixed) {
@@ -586,7 +614,8 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
                     pw = pow_fwd<true, STRIDE>(1.0 - v[c][1], g.lnf_hi[i], g.lnf_lo[i], tab);
                     ipw = fast_rcp(pw);
                 }
-                dynamic_quad_terms_r(n1, n2, e1, e2, v[c][1], v[c][0] * ipw, pw * ia[c], T, t.c0, t.a1, t.a2);
+                dynamic_quad_terms_k(f1[c], f2[c], g1[c], g2[c], v[c][1], v[c][0] * ipw, pw * ia[c], T, t.c0, t.a1,
+                                     t.a2);
             }
             out[c] += qr_cost(t, f);
         }
