@@ -367,8 +367,9 @@ SABR_HD double bitsd(uint64_t u) {
 // hi is exact) + lo} (host long double,
 // kernels_mc.cu: log_table_host()); the two intervals around 1 (kLogOne - 1,
 // kLogOne) have invc = 1, -log(invc) = 0, so r = z - 1 exactly and nothing
-// cancels as log x -> 0.  <= 1 ulp (tools/mathtab_check.cpp); 16 FP64 ops, no
-// branch (libdevice log: 31 FP64 ops, 104 instructions).
+// cancels as log x -> 0.  <= 1 ulp (0.72, tools/mathtab_check.cpp) with the
+// series to r^7 (r^8/8 < 2^-60 here; r02: the r^8 term dropped); 15 FP64
+// ops, no branch (libdevice log: 31 FP64 ops, 104 instructions).
 constexpr int kLogTableSize = 128;
 constexpr int kLogOne = 80;  // the interval that starts at z = 1: (bits(1) - bits(0.6875)) >> 45
 
@@ -388,14 +389,17 @@ SABR_HD double log_tab(double x, const double4* __restrict__ tab) {
     const double t2 = t1 + r;
     const double lo = fma(kd, kLn2Lo, e.z) + ((t1 - t2) + r);
     const double r2 = r * r;
-    const double p = fma(fma(fma(fma(fma(fma(fma(-1.0 / 8, r, 1.0 / 7), r, -1.0 / 6), r, 1.0 / 5), r, -1.0 / 4),
-                                     r, 1.0 / 3), r, -0.5), r2, lo);
+    const double p = fma(fma(fma(fma(fma(fma(1.0 / 7, r, -1.0 / 6), r, 1.0 / 5), r, -1.0 / 4), r, 1.0 / 3), r, -0.5),
+                         r2, lo);
     return t2 + p;
 }
 
-// sqrt(a) for a >= 0 (finite): MUFU.RSQ64H seed, two Goldschmidt steps and a
-// final residual correction (<= 1 ulp; libdevice's IEEE sqrt has a slow-path
-// branch and 24 FP64 ops).  sqrt(0) = 0.
+// sqrt(a) for a >= 0 (finite): MUFU.RSQ64H seed, one Goldschmidt step and a
+// final residual correction: the step takes the ~2^-23 seed to ~2^-46, the
+// correction (with the residual a - s^2 formed exactly by an FMA) to full
+// precision, 0.5 ulp (tools/mathtab_check.cpp; r02: the second Goldschmidt
+// step was redundant); libdevice's IEEE sqrt has a slow-path branch and 24
+// FP64 ops.  sqrt(0) = 0.
 SABR_HD double sqrt_pos(double a) {
 #ifdef __CUDA_ARCH__
     double y;
@@ -405,10 +409,7 @@ SABR_HD double sqrt_pos(double a) {
     const double y = bitsd(dbits(1.0 / __builtin_sqrt(a)) & ~((1ull << 29) - 1));
 #endif
     double s = a * y, h = 0.5 * y;
-    double r = fma(-s, h, 0.5);
-    s = fma(s, r, s);
-    h = fma(h, r, h);
-    r = fma(-s, h, 0.5);
+    const double r = fma(-s, h, 0.5);
     s = fma(s, r, s);
     h = fma(h, r, h);
     const double d = fma(-s, s, a);
@@ -420,7 +421,8 @@ SABR_HD double sqrt_pos(double a) {
 // x = 128 u (exact), k = rint(x), f = x - k in [-1/2, 1/2] (exact); table
 // entry k mod 128 = {sin(pi k/64), cos(pi k/64)} (host long double,
 // kernels_mc.cu: sincos_table_host()); t = (pi/64) f in double-double
-// precision, sin t and cos t - 1 by Taylor polynomials (truncation < 1e-22
+// precision, sin t and cos t - 1 by Taylor polynomials to t^7 / t^6 (r02;
+// truncation < 1e-20
 // for |t| <= pi/128); recombined by the angle-addition formulas.
 // <= 1 ulp (tools/mathtab_check.cpp); branch-free (libdevice sincospi: 96
 // instructions).
@@ -436,9 +438,9 @@ SABR_HD void sincos_2pi(double u, const double2* __restrict__ tab, double& s, do
     const int k = static_cast<int>(kd) & (kSinCosTableSize - 1);
     const double t = fma(f, kPi64Hi, f * kPi64Lo);
     const double t2 = t * t;
-    const double ps = fma(fma(fma(t2, 1.0 / 362880, -1.0 / 5040), t2, 1.0 / 120), t2, -1.0 / 6);
+    const double ps = fma(fma(t2, -1.0 / 5040, 1.0 / 120), t2, -1.0 / 6);
     const double st = fma(t * t2, ps, t);
-    const double pc = fma(fma(fma(t2, 1.0 / 40320, -1.0 / 720), t2, 1.0 / 24), t2, -0.5);
+    const double pc = fma(fma(t2, -1.0 / 720, 1.0 / 24), t2, -0.5);
     const double cm1 = t2 * pc;
     const double2 e = tab[k];
     s = e.x + fma(e.x, cm1, e.y * st);
