@@ -300,6 +300,26 @@ SABR_D double exp_mc(double x, const double2* __restrict__ tab) {
     return fabs(x) > 700.0 ? sat : res;
 }
 
+// case2_mc_cost's sum over one candidate's quotes, calibration.cpp:410-413:
+// the reference's sequential order; 8 quotes' loads and divisions are
+// independent and issued together (C5: 600 quotes per candidate)
+SABR_D double mc_quote_cost(const double* __restrict__ v, const double* __restrict__ market, int nq) {
+    double sum = 0.0;
+    int q = 0;
+    for (; q + 8 <= nq; q += 8) {
+        double rel[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rel[u] = (market[q + u] - v[q + u]) / market[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += rel[u] * rel[u];
+    }
+    for (; q < nq; ++q) {
+        const double rel = (market[q] - v[q]) / market[q];
+        sum += rel * rel;
+    }
+    return sum;
+}
+
 // ----------------------------------------------------------- Metropolis ---
 // annealer.cpp:125-126: accept iff fy <= fx || u < exp(-(fy - fx) / T), with
 // u = uniform() drawn only when fy > fx.  With tau = -ln u the test is

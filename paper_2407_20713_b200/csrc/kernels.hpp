@@ -149,6 +149,10 @@ struct T2StepArgs {
     int64_t level;
 };
 
+// one MC launch per step: cost + scatter + Metropolis in one kernel (t2_finish_kernel)
+cudaError_t launch_t2_finish(T2Chain* chains, const T2StepArgs& a, const int32_t* idx, const int32_t* n_live,
+                             const double* values, int32_t nq, const double* market, const int* bad_c,
+                             int* nonfinite, cudaStream_t s);
 cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
                                  cudaStream_t s);
 // propose + feasibility (analytics.cpp:145-175 on the grid), writes the MC

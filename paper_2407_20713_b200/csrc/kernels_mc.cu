@@ -646,24 +646,9 @@ __global__ void mc_cost_kernel(const McParams P, const double* __restrict__ valu
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P.n_cand) return;
     if (P.active != nullptr && P.active[c] == 0) return;
-    // the reference's sequential order; 8 quotes' loads and divisions are
-    // independent and issued together (C5: 600 quotes per candidate)
-    const double* v = value + static_cast<int64_t>(c) * P.n_quotes;
-    double sum = 0.0;
-    int q = 0;
-    for (; q + 8 <= P.n_quotes; q += 8) {
-        double rel[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) rel[u] = (market[q + u] - v[q + u]) / market[q + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) sum += rel[u] * rel[u];
-    }
-    for (; q < P.n_quotes; ++q) {
-        const double rel = (market[q] - v[q]) / market[q];
-        sum += rel * rel;
-    }
-    cost[c] = sum;
+    cost[c] = mc_quote_cost(value + static_cast<int64_t>(c) * P.n_quotes, market, P.n_quotes);
 }
+
 
 template <int CB>
 cudaError_t tiles_t(const McParams& p, cudaStream_t s) {

@@ -1688,15 +1688,8 @@ __global__ void t2_scatter_kernel(const int32_t* __restrict__ idx, const int32_t
     bad[c] |= bad_c[k];
 }
 
-__global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
-                                 const double* __restrict__ cost, const int* __restrict__ bad,
-                                 int* __restrict__ nonfinite) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= a.n_local) return;
-    T2Chain& ch = chains[c];
-    if (!ch.active) return;
-    if (bad[c]) atomicOr(nonfinite, 1);
-    double fy = cost[c];
+// Metropolis for one chain's evaluated proposal (annealer.cpp:122-133)
+__device__ __forceinline__ void t2_accept_one(T2Chain& ch, double fy, const T2StepArgs& a) {
     if (isnan(fy)) fy = CUDART_INF;
     ch.evals += 1;
     bool accept = fy <= ch.fx;
@@ -1714,6 +1707,32 @@ __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs 
             for (int i = 0; i < 10; ++i) ch.bp[i] = ch.y[i];
         }
     }
+}
+
+__global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
+                                 const double* __restrict__ cost, const int* __restrict__ bad,
+                                 int* __restrict__ nonfinite) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.n_local) return;
+    T2Chain& ch = chains[c];
+    if (!ch.active) return;
+    if (bad[c]) atomicOr(nonfinite, 1);
+    t2_accept_one(ch, cost[c], a);
+}
+
+// A step whose candidates are one MC launch (r02): the candidate's cost
+// (mc_cost_kernel's sum), its chain (t2_scatter) and the Metropolis test
+// (t2_accept) in one kernel, one thread per compacted candidate - the same
+// arithmetic, two launches fewer per SA step.
+__global__ void t2_finish_kernel(T2Chain* __restrict__ chains, const T2StepArgs a, const int32_t* __restrict__ idx,
+                                 const int32_t* __restrict__ n_live, const double* __restrict__ values,
+                                 const int32_t nq, const double* __restrict__ market,
+                                 const int* __restrict__ bad_c, int* __restrict__ nonfinite) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= *n_live) return;
+    T2Chain& ch = chains[idx[k]];
+    if (bad_c[k]) atomicOr(nonfinite, 1);
+    t2_accept_one(ch, mc_quote_cost(values + static_cast<int64_t>(k) * nq, market, nq), a);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -2094,6 +2113,15 @@ cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double*
                              const int* bad, int* nonfinite, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
     t2_accept_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, a, cost, bad, nonfinite);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_t2_finish(T2Chain* chains, const T2StepArgs& a, const int32_t* idx, const int32_t* n_live,
+                             const double* values, int32_t nq, const double* market, const int* bad_c,
+                             int* nonfinite, cudaStream_t s) {
+    if (a.n_local <= 0) return cudaSuccess;
+    t2_finish_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, a, idx, n_live, values, nq, market, bad_c,
+                                                             nonfinite);
     return cudaGetLastError();
 }
 

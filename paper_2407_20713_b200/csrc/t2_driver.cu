@@ -201,6 +201,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     ta.seed = sch.seed;
     ta.chain_begin = begin;
 
+    const bool one_chunk = n_local <= chunk;
     Timer timer(ctx);
     timer.start();
     int64_t mc_launches = 0, launches = 0;
@@ -243,14 +244,23 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
                     const size_t slab = sizeof(double) * 2 * static_cast<size_t>(tpr) * nc * nq;
                     allgather(ctx, reinterpret_cast<unsigned char*>(partials) + ctx->rank * slab, partials, slab);
                 }
-                check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, cost_c + c0, ctx->stream), "mc_reduce");
+                // one chunk (the step's candidates in one MC launch): the cost, the
+                // scatter and the Metropolis test are one kernel (t2_finish)
+                check_cuda(launch_mc_reduce(Q, values, nullptr, d_market, one_chunk ? nullptr : cost_c + c0,
+                                            ctx->stream), "mc_reduce");
                 mc_launches += 1;
-                launches += 4;
+                launches += one_chunk ? 3 : 4;
             }
-            check_cuda(launch_t2_scatter(cidx, n_live, n_local, cost_c, bad_c, cost, bad, ctx->stream), "t2_scatter");
-            launches += 2;
-            check_cuda(launch_t2_accept(chains, ta, cost, bad, nonfinite, ctx->stream), "t2_accept");
-            launches += 2;
+            if (one_chunk) {
+                check_cuda(launch_t2_finish(chains, ta, cidx, n_live, values, nq, d_market, bad_c, nonfinite,
+                                            ctx->stream), "t2_finish");
+                launches += 1;
+            } else {
+                check_cuda(launch_t2_scatter(cidx, n_live, n_local, cost_c, bad_c, cost, bad, ctx->stream),
+                           "t2_scatter");
+                check_cuda(launch_t2_accept(chains, ta, cost, bad, nonfinite, ctx->stream), "t2_accept");
+                launches += 2;
+            }
         }
         check_cuda(launch_t2_level_end(chains, a, level, ctx->stream), "t2_level_end");
         if (a.nranks > 1) {
