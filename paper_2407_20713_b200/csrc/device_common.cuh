@@ -497,11 +497,11 @@ SABR_D void box_muller_tab(double ua, double ub, const double4* __restrict__ log
 // and exactly 2^64 -> u1 = 1 for U1 = 0), r = sqrt(-2 ln2 lg2 u1), theta =
 // 2 pi U2 taken to [-pi, pi) for sin/cos.approx.  Absolute errors ~1e-6 in
 // the normals (lg2/sin/cos.approx ~2^-21), far inside the FP32 path's 2e-5
-// price tolerance; one LG2, one SQRT, one SIN, one COS and two I2F instead of
+// price tolerance; one LG2, one SQRT, one SIN, one COS and one I2F instead of
 // libm's logf/sqrtf/sincospif (~150 instructions per path-step with their
 // range reductions and slow-path calls).
 SABR_D void box_muller_f32_bits(uint64_t n1, uint64_t n2, float& z1, float& z2) {
-    const uint64_t m1 = n1 & ~0x7ffull, m2 = n2 & ~0x7ffull;
+    const uint64_t m1 = n1 & ~0x7ffull;
     float lg, r, sn, cs;
     // lg2 of u1 itself (in [2^-53, 1]), not of the 2^64-scaled integer: the
     // result is near 0 when u1 is near 1 (small r), where float resolves it
@@ -510,8 +510,13 @@ SABR_D void box_muller_f32_bits(uint64_t n1, uint64_t n2, float& z1, float& z2) 
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(__ull2float_rn(~m1) * 0x1.0p-64f));
     const float w = -1.38629436f * lg;  // -2 ln u1 >= 0
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(w));
-    const float u2 = __ull2float_rn(m2) * 0x1.0p-64f;
-    const float t = (u2 >= 0.5f ? u2 - 1.0f : u2) * 6.28318531f;  // 2 pi U2 in [-pi, pi)
+    // U2 taken to [-1/2, 1/2) without a conversion (r02, one XU instruction
+    // fewer): its top 23 bits with the top one flipped are the mantissa of a
+    // float in [1, 2), which minus 1.5 (exactly) is U2 or U2 - 1 truncated to
+    // 2^-23; the half-step 2^-24 folded into the angle's FMA centres the
+    // grid, so the angle is within 2 pi 2^-24 of 2 pi U2
+    const float v2 = __uint_as_float(static_cast<uint32_t>(n2 >> 41) ^ 0x3fc00000u) - 1.5f;
+    const float t = fmaf(v2, 6.28318531f, 6.28318531f * 0x1.0p-24f);  // 2 pi U2 in [-pi, pi)
     asm("sin.approx.ftz.f32 %0, %1;" : "=f"(sn) : "f"(t));
     asm("cos.approx.ftz.f32 %0, %1;" : "=f"(cs) : "f"(t));
     z1 = r * cs;
