@@ -1047,6 +1047,8 @@ void mc_price_single(sabr_ctx* ctx, int model, const double* params, double spot
     check_cuda(cudaMemsetAsync(P.bad, 0, sizeof(int), ctx->stream), "memset bad");
     double* dv = static_cast<double*>(dev_buf(ctx, "mc_value", sizeof(double) * nq));
     double* ds = static_cast<double*>(dev_buf(ctx, "mc_se", sizeof(double) * nq));
+    if (mc_max_cand_block(P.max_q, P.fp32 != 0) == 0)
+        fail(SABR_E_RUNTIME, "price_european_batch: too many strikes in one slice for the MC tile kernel");
     Timer timer(ctx);
     timer.start();
     timer.before();

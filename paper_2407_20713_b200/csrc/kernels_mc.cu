@@ -683,6 +683,23 @@ cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
 
 }  // namespace
 
+// Shared memory of one tile CTA at CB candidates and max_q quotes per slice:
+// the warps' payoff accumulators and transpose tiles (dynamic) plus, in FP64,
+// the exp / log / sincos tables (static), against the 227 KB a CTA can opt in
+// to.  The largest CB that fits, 0 when even one candidate does not.
+int mc_max_cand_block(int max_q, bool fp32) {
+    constexpr size_t kLimit = 227 * 1024;
+    const size_t tables = fp32 ? 0
+                               : sizeof(double2) * kExpTableSize * kExpRep + sizeof(double4) * kLogTableSize +
+                                     sizeof(double2) * kSinCosTableSize;
+    for (int cb : {16, 8, 4, 2, 1}) {
+        const size_t dyn = (static_cast<size_t>(kWarps) * cb * max_q * 2 + static_cast<size_t>(kWarps) * 32 * kTrStride) *
+                           sizeof(double);
+        if (tables + dyn + 1024 <= kLimit) return cb;
+    }
+    return 0;
+}
+
 cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s) {
     switch (cand_block) {
         case 1: return tiles_t<1>(p, s);

@@ -92,6 +92,9 @@ constexpr int kMcThreads = 128;
 // Simulate + fused payoff reduction per tile (price_european_batch,
 // mc.cpp:249-273) or terminal write (simulate_terminals, mc.cpp:231-240).
 cudaError_t launch_mc_tiles(const McParams& p, int cand_block, cudaStream_t s);
+// the largest candidate block (16, 8, 4, 2, 1) whose tile CTA fits in shared
+// memory at max_q quotes per slice; 0 when none does
+int mc_max_cand_block(int max_q, bool fp32);
 
 // Final fixed-order reduction over tiles -> value/std_error per (cand, quote)
 // (reduce_payoffs, mc.cpp:146-157); optional cost per candidate against

@@ -106,6 +106,10 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) cb = v;
     }
+    // the payoff accumulators of a tile CTA grow with CB x quotes per slice
+    const int cb_fit = mc_max_cand_block(job.max_q, fp32);
+    if (cb_fit == 0) fail(SABR_E_RUNTIME, "case2_mc_cost: too many quotes in one slice for the MC tile kernel");
+    while (cb > cb_fit) cb /= 2;
     const int32_t stride = (chunk + cb - 1) / cb * cb;  // coefficient row width
 
     McParams P{};

@@ -186,3 +186,22 @@ def test_case2_T2_candidate_block_invariance(engine, eq_surface, precision, case
         assert b.final_cost == a.final_cost, (cb, b.final_cost, a.final_cost)
         assert b.params == a.params, cb
         assert b.temperature_trace == a.temperature_trace, cb
+
+
+def test_case2_T2_wide_slice_matches_reference(engine, ref):
+    """A slice of 400 quotes: the tile kernel's payoff accumulators outgrow
+    shared memory at 8 or 16 candidates per thread, so the engine drops to the
+    largest block that fits (kernels_mc.cu mc_max_cand_block); results as the
+    reference's."""
+    K = np.linspace(60.0, 140.0, 400)
+    quotes = [pkg.VolQuote(float(k), float(0.2 + 0.1 * (k / 100.0 - 1.0) ** 2)) for k in K]
+    surf = pkg.VolSurface(100.0, [pkg.VolSlice(1.0, 0.01, 0.0, quotes)])
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=2, workers=16, t_min=0.9, seed=6)
+    plan = pkg.SimulationPlan(num_paths=512, seed=3)
+    g = engine.calibrate_case2_T2(surf, None, s, plan, fixed)
+    r = ref.calibrate_case2_T2(surf, None, s, plan, fixed)
+    assert g.evals == r.evals
+    assert abs(g.final_cost - r.final_cost) <= 1e-9 * r.final_cost
+    for k in r.params:
+        assert abs(g.params[k] - r.params[k]) <= 1e-7 * max(1.0, abs(r.params[k])), k
