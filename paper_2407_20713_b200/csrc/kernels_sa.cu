@@ -443,15 +443,50 @@ __device__ __forceinline__ double qr_cost(const QuadTerms& t, const QrFactor& f)
     return fma(u0, u0, fma(u1, u1, fma(u2, u2, f.r33sq)));
 }
 
-__device__ __forceinline__ QuadTerms static_qterms(const double* v, double pw, double T) {
+struct QrSlice {  // the static objective's slice, hoisted into registers
+    double lnf_hi, lnf_lo, T24, T4;  // T/24, T/4
+    QrFactor f;                      // R with columns 1, 2 scaled by -1/2, 1/12 (static_qterms_f)
+};
+
+// The static slice with the constants of static_quad_terms folded in (r02):
+// A1/omega = -p/2 and A2/omega = X/12 enter ||R v||^2 through R's columns 1
+// and 2 (scaled once per CTA: -1/2 exactly, 1/12 within an ulp), and B T
+// is formed directly with T/24 and T/4: three FP64 instructions fewer per eval.
+__device__ __forceinline__ QrSlice qr_slice(const QGrid& g) {
+    QrFactor f = load_qr(g.R);
+    f.r01 *= -0.5;
+    f.r11 *= -0.5;
+    f.r02 *= (1.0 / 12.0);
+    f.r12 *= (1.0 / 12.0);
+    f.r22 *= (1.0 / 12.0);
+    const double T = g.T[0];
+    return QrSlice{g.lnf_hi[0], g.lnf_lo[0], T * (1.0 / 24.0), T * 0.25, f};
+}
+
+// static_quad_terms with the folded slice: (C0, p, X) for qr_cost on the
+// folded factor (C0 = 1/omega + (1/omega) B T as before)
+__device__ __forceinline__ QuadTerms static_qterms_f(const double* v, double pw, const QrSlice& sl) {
+    const double alpha = v[0], beta = v[1], nu = v[2], rho = v[3];  // (alpha, beta, nu, rho): static_quad_terms
+    const double omb = 1.0 - beta;
+    const double r = fast_rcp(alpha * pw);
+    const double inv = alpha * (alpha * r);  // 1/omega
+    const double omega = pw * (pw * r);
+    const double rn = rho * nu;
+    const double q = omb * inv;
+    const double p = q - rn;
+    const double rrn2 = fma(-3.0 * rho, rho, 2.0) * (nu * nu);
     QuadTerms t;
-    static_quad_terms(v[0], v[1], v[2], v[3], pw, T, t.c0, t.a1, t.a2);
+    t.a1 = p;
+    t.a2 = fma(rrn2, omega, fma(3.0, p, omb * q));
+    const double BT = fma(q * sl.T24, q, fma((sl.T4 * beta) * rn, inv, rrn2 * sl.T24));
+    t.c0 = fma(inv, BT, inv);
     return t;
 }
 
 __device__ __forceinline__ double static_cost(const double* v, const QGrid& g) {
-    const double pw = pow_fwd(1.0 - v[1], g.lnf_hi[0], g.lnf_lo[0], g.tab);
-    return qr_cost(static_qterms(v, pw, g.T[0]), load_qr(g.R));
+    const QrSlice sl = qr_slice(g);
+    const double pw = pow_fwd(1.0 - v[1], sl.lnf_hi, sl.lnf_lo, g.tab);
+    return qr_cost(static_qterms_f(v, pw, sl), sl.f);
 }
 
 // Per-vector constants of the Case I closed forms' scale factors (r02): with
@@ -506,14 +541,6 @@ __device__ __forceinline__ double case1_cost(const double* v, const QGrid& g) {
     return sum;
 }
 
-struct QrSlice {  // the static objective's slice, hoisted into registers
-    double lnf_hi, lnf_lo, T;
-    QrFactor f;
-};
-
-__device__ __forceinline__ QrSlice qr_slice(const QGrid& g) {
-    return QrSlice{g.lnf_hi[0], g.lnf_lo[0], g.T[0], load_qr(g.R)};
-}
 
 template <int C, int DIMF, bool FAST, int STRIDE = 1>
 __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const QrSlice& sl,
@@ -521,7 +548,7 @@ __device__ __forceinline__ void static_cost_n(const double (&v)[C][DIMF], const 
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const double pw = pow_fwd<!FAST, STRIDE>(1.0 - v[c][1], sl.lnf_hi, sl.lnf_lo, tab);
-        out[c] = qr_cost(static_qterms(v[c], pw, sl.T), sl.f);
+        out[c] = qr_cost(static_qterms_f(v[c], pw, sl), sl.f);
     }
 }
 
