@@ -18,7 +18,7 @@ for e in engs:
     e.set_profiling(True)
 fx = pkg.parse_surface(os.path.join(ROOT, "tests", "data", "eurusd.csv"))
 s = pkg.AnnealingSchedule(t0=2.0, cooling=0.96, chain_length=100, workers=12_500, groups=8,
-                          t_min=2.0 * 0.96 ** 19 * 0.999, max_evals=10 ** 12, seed=1)
+                          t_min=float(os.environ.get("AB_TMIN", 2.0 * 0.96 ** 19 * 0.999)), max_evals=10 ** 12, seed=1)
 
 
 def run(e, what):
