@@ -677,54 +677,22 @@ SABR_HD SmileTerms static_terms(double alpha, double beta, double nu, double rho
     return t;
 }
 
-// static_terms folded into the three terms of the factored cost,
-// x = (C0, A1, A2) = (1 + B T, A1, A2) / omega, regrouped in powers of
-// 1/omega (q = (1-beta)/omega, p = q - rho nu = A1-part):
+// The factored cost's terms: static_terms / dynamic_terms folded into
+// x = (C0, A1, A2) = (1 + B T, A1, A2) / omega and regrouped in powers of
+// 1/omega (q = (1-beta)/omega; static: p = q - rho nu, Case I: p = q - eta1):
 //     A1/omega = -p/2
-//     A2/omega = ((1-beta) q + 3 p + (2 - 3 rho^2) nu^2 omega) / 12
-//     B        = q^2/24 + beta rho nu / (4 omega) + (2 - 3 rho^2) nu^2 / 24
+//     A2/omega = static: ((1-beta) q + 3 p + (2 - 3 rho^2) nu^2 omega) / 12
+//                Case I: (1-beta) q / 12 + p / 4 + (4 nu1^2 + 3 (eta2^2 - 3 eta1^2)) omega / 24
+//     B        = static: q^2/24 + beta rho nu / (4 omega) + (2 - 3 rho^2) nu^2 / 24
+//                Case I: q^2/24 + beta eta1 / (4 omega) + (2 nu2^2 - 3 eta2^2) / 24
 //     C0       = 1/omega + (1/omega) B T
-// with one reciprocal of alpha f^(1-beta) for both omega and 1/omega
-// (30 FP64 instructions instead of 44).  Each term is within a few ulp of
-// the reference's value; the factored cost's own conditioning dominates.
-SABR_HD void static_quad_terms(double alpha, double beta, double nu, double rho, double pw, double T,
-                               double& c0, double& a1, double& a2) {
-    const double omb = 1.0 - beta;
-    const double r = fast_rcp(alpha * pw);
-    const double inv = alpha * (alpha * r);  // 1/omega
-    const double omega = pw * (pw * r);
-    const double rn = rho * nu;
-    const double q = omb * inv;
-    const double p = q - rn;
-    const double rrn2 = fma(-3.0 * rho, rho, 2.0) * (nu * nu);
-    a1 = -0.5 * p;
-    a2 = fma(rrn2, omega, fma(3.0, p, omb * q)) * (1.0 / 12.0);
-    const double B = fma(q * (1.0 / 24.0), q, fma((0.25 * beta) * rn, inv, rrn2 * (1.0 / 24.0)));
-    c0 = fma(inv, B * T, inv);
-}
+// with one reciprocal of alpha f^(1-beta) for both omega and 1/omega.  Each
+// term is within a few ulp of the reference's value; the factored cost's own
+// conditioning dominates.  The static form with its constants folded into the
+// slice factor is kernels_sa.cu static_qterms_f; the Case I form on the scaled
+// functionals is dynamic_quad_terms_k below.
 
-// dynamic_terms (below) folded into the terms of the factored cost like
-// static_quad_terms, with q = (1-beta)/omega and p = q - eta1:
-//     A1/omega = -p/2
-//     A2/omega = (1-beta) q / 12 + p / 4 + (4 nu1^2 + 3 (eta2^2 - 3 eta1^2)) omega / 24
-//     B        = q^2/24 + beta eta1 / (4 omega) + (2 nu2^2 - 3 eta2^2) / 24
-//     C0       = 1/omega + (1/omega) B T
-SABR_HD void dynamic_quad_terms(double nu1_sq, double nu2_sq, double eta1, double eta2_sq, double alpha,
-                                double beta, double pw, double T, double& c0, double& a1, double& a2) {
-    const double omb = 1.0 - beta;
-    const double r = fast_rcp(alpha * pw);
-    const double inv = alpha * (alpha * r);
-    const double omega = pw * (pw * r);
-    const double q = omb * inv;
-    const double p = q - eta1;
-    const double k = fma(4.0, nu1_sq, 3.0 * fma(-3.0 * eta1, eta1, eta2_sq));
-    a1 = -0.5 * p;
-    a2 = fma(k * (1.0 / 24.0), omega, fma(0.25, p, (omb * q) * (1.0 / 12.0)));
-    const double B = fma(q * (1.0 / 24.0), q, fma((0.25 * beta) * eta1, inv, fma(2.0, nu2_sq, -3.0 * eta2_sq) * (1.0 / 24.0)));
-    c0 = fma(inv, B * T, inv);
-}
-
-// The Case I terms of the factored cost (dynamic_quad_terms) written on the
+// The Case I terms of the factored cost written on the
 // scaled functionals of a slice (r02),
 //     Af1 = nu0^2/6 f_nu1,  Ef2 = nu0^2/12 f_nu2,  dg1 = nu0 rho0/4 f_eta1 = eta1/4,
 //     bg2 = (nu0 rho0)^2/8 f_eta2 = eta2^2/8,
@@ -803,25 +771,9 @@ __device__ __forceinline__ void case1_series_pair(double x, const double* __rest
     g = horner_s(ser, 2 * PAIR + 1, x);
 }
 
-template <int PAIR, int STRIDE = 1>
-__device__ __forceinline__ void case1_closed_pair(double x, const double2* __restrict__ tab, double& f,
-                                                  double& g) {
-    const double e = exp_tab<STRIDE>(-x, tab);
-    const double x2 = SABR_MUL(x, x);
-    if constexpr (PAIR == 0) {
-        const double c6 = 6.0 * fast_rcp(SABR_MUL(x2, x));
-        f = SABR_MUL(c6, SABR_SUB(SABR_ADD(SABR_SUB(SABR_MUL(x2, 0.5), x), 1.0), e));
-        g = SABR_MUL(c6, SABR_ADD(SABR_MUL(2.0, SABR_SUB(e, 1.0)), SABR_MUL(x, SABR_ADD(e, 1.0))));
-    } else {
-        f = SABR_MUL(2.0 * fast_rcp(x2), SABR_SUB(e, SABR_SUB(1.0, x)));
-        const double x4 = SABR_MUL(SABR_MUL(x2, x), x);
-        const double poly = SABR_ADD(SABR_ADD(SABR_SUB(SABR_MUL(e, e), SABR_MUL(8.0, e)), 7.0),
-                                     SABR_MUL(SABR_MUL(2.0, x), SABR_SUB(x, 3.0)));
-        g = SABR_MUL(3.0 * fast_rcp(x4), poly);
-    }
-}
-
-// case1_closed_pair with its scale factors supplied (sa, sb within a few ulp
+// The closed forms of one functional pair (f_nu1/f_nu2 at x = 2bT: PAIR 0;
+// f_eta1/f_eta2 at x = (a+b)T: PAIR 1), analytics.cpp:46-67, with their
+// scale factors supplied (sa, sb within a few ulp
 // of the quotients times the chain's constants, case1_scales): PAIR 0 takes
 // sa ~ nu0^2 / x^3 and sb ~ nu0^2 / (2 x^3), PAIR 1 sa ~ nu0 rho0 / (2 x^2) and
 // sb ~ 3 (nu0 rho0)^2 / (8 x^4).  The brackets are the reference's
@@ -855,9 +807,9 @@ __device__ __forceinline__ void case1_closed_pair_r(double x, double sa, double 
 // same branch (the rule late in a schedule, when the chains cluster), their
 // evaluations share one branch body and interleave (C-fold ILP); mixed
 // threads evaluate chain by chain.  Per-chain results do not depend on C.
-// RCP: the closed forms take their scale factors from sa, sb (case1_closed_pair_r)
-// (the series values times ca, cb: the chain's constants of case1_scales)
-template <int PAIR, int C, int STRIDE = 1, bool RCP = false>
+// The closed forms take their scale factors from sa, sb; the series values
+// are multiplied by ca, cb (the chains' constants, case1_series_consts).
+template <int PAIR, int C, int STRIDE = 1>
 __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double* __restrict__ ser,
                                              const double2* __restrict__ tab, double (&f)[C], double (&g)[C],
                                              const double (&sa)[C], const double (&sb)[C],
@@ -873,28 +825,22 @@ __device__ __forceinline__ void case1_pair_n(const double (&x)[C], const double*
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
-            if constexpr (RCP) {
-                f[c] *= ca[c];
-                g[c] *= cb[c];
-            }
+            f[c] *= ca[c];
+            g[c] *= cb[c];
         }
     } else if (all_closed) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
-            else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
-        }
+        for (int c = 0; c < C; ++c) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
     } else {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if (x[c] < kXSwitch) {
                 case1_series_pair<PAIR>(x[c], ser, f[c], g[c]);
-                if constexpr (RCP) {
-                    f[c] *= ca[c];
-                    g[c] *= cb[c];
-                }
-            } else if constexpr (RCP) case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
-            else case1_closed_pair<PAIR, STRIDE>(x[c], tab, f[c], g[c]);
+                f[c] *= ca[c];
+                g[c] *= cb[c];
+            } else {
+                case1_closed_pair_r<PAIR, STRIDE>(x[c], sa[c], sb[c], tab, f[c], g[c]);
+            }
         }
     }
 }
@@ -916,8 +862,8 @@ __device__ __forceinline__ void case1_functionals(double a, double b, double T, 
     const double s0[1] = {sc[0]}, s1[1] = {sc[1]}, s2[1] = {sc[2]}, s3[1] = {sc[3]};
     const double c0[1] = {cs[0]}, c1[1] = {cs[1]}, c2[1] = {cs[2]}, c3[1] = {cs[3]};
     double F1[1], F2[1], G1[1], G2[1];
-    case1_pair_n<0, 1, 1, true>(xb, ser, tab, F1, F2, s0, s1, c0, c1);
-    case1_pair_n<1, 1, 1, true>(xab, ser, tab, G1, G2, s2, s3, c2, c3);
+    case1_pair_n<0, 1, 1>(xb, ser, tab, F1, F2, s0, s1, c0, c1);
+    case1_pair_n<1, 1, 1>(xab, ser, tab, G1, G2, s2, s3, c2, c3);
     Af1 = F1[0];
     Ef2 = F2[0];
     dg1 = G1[0];

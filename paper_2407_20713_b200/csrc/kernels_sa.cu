@@ -448,7 +448,7 @@ struct QrSlice {  // the static objective's slice, hoisted into registers
     QrFactor f;                      // R with columns 1, 2 scaled by -1/2, 1/12 (static_qterms_f)
 };
 
-// The static slice with the constants of static_quad_terms folded in (r02):
+// The static slice with the constants of the static terms folded in (r02):
 // A1/omega = -p/2 and A2/omega = X/12 enter ||R v||^2 through R's columns 1
 // and 2 (scaled once per CTA: -1/2 exactly, 1/12 within an ulp), and B T
 // is formed directly with T/24 and T/4: three FP64 instructions fewer per eval.
@@ -463,10 +463,10 @@ __device__ __forceinline__ QrSlice qr_slice(const QGrid& g) {
     return QrSlice{g.lnf_hi[0], g.lnf_lo[0], T * (1.0 / 24.0), T * 0.25, f};
 }
 
-// static_quad_terms with the folded slice: (C0, p, X) for qr_cost on the
-// folded factor (C0 = 1/omega + (1/omega) B T as before)
+// The static terms (device_common.cuh: the factored cost's terms) on the
+// folded slice: (C0, p, X) for qr_cost on the folded factor
 __device__ __forceinline__ QuadTerms static_qterms_f(const double* v, double pw, const QrSlice& sl) {
-    const double alpha = v[0], beta = v[1], nu = v[2], rho = v[3];  // (alpha, beta, nu, rho): static_quad_terms
+    const double alpha = v[0], beta = v[1], nu = v[2], rho = v[3];  // the static vector (alpha, beta, nu, rho)
     const double omb = 1.0 - beta;
     const double r = fast_rcp(alpha * pw);
     const double inv = alpha * (alpha * r);  // 1/omega
@@ -624,8 +624,8 @@ __device__ __forceinline__ void case1_cost_n(const double (&v)[C][DIMF], const Q
                 ca1[c] = cs[2];
                 cb1[c] = cs[3];
             }
-            case1_pair_n<0, C, STRIDE, true>(xb, g.ser, tab, f1, f2, sa0, sb0, ca0, cb0);
-            case1_pair_n<1, C, STRIDE, true>(xab, g.ser, tab, g1, g2, sa1, sb1, ca1, cb1);
+            case1_pair_n<0, C, STRIDE>(xb, g.ser, tab, f1, f2, sa0, sb0, ca0, cb0);
+            case1_pair_n<1, C, STRIDE>(xab, g.ser, tab, g1, g2, sa1, sb1, ca1, cb1);
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
