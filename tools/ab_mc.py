@@ -31,7 +31,7 @@ libs = sys.argv[1:]
 engs = [pkg.Engine(0, lib=_abi.load_library(p)) for p in libs]
 for what in ("c4", "c5"):
     for precision in ("fp64", "fp32"):
-        vals = [[], []]
+        vals = [[] for _ in engs]
         for _ in range(3):
             for i, e in enumerate(engs):
                 vals[i].append(run(e, what, precision))
