@@ -47,7 +47,11 @@ def main(tag, copy=("sa", "case1", "t2", "t2_fp32", "mc", "mc_fp32", "c5", "c5_f
          "mc_single_fp64_pipe_instr_per_path_step": mc[4]}
     f32 = os.path.join(src, "ncu_metrics_t2_fp32.csv")
     if os.path.exists(f32):  # the FP32 MC path: MUFU (XU) instructions per candidate-path-step
-        t2f = per(f32, "mc_tile_kernel_f32<8", 32 * 1e5 * 250)
+        # C4 FP32 runs 16 candidates per thread (time-invariant rows), earlier builds 8
+        try:
+            t2f = per(f32, "mc_tile_kernel_f32<16", 32 * 1e5 * 250)
+        except IndexError:
+            t2f = per(f32, "mc_tile_kernel_f32<8", 32 * 1e5 * 250)
         d["c4_fp32_xu_instr_per_candidate_path_step"] = t2f[6]
         d["c4_fp32_mc_kernel_ns"] = t2f[3]
         d["c4_fp32_warp_instr_per_candidate_path_step"] = t2f[5]
