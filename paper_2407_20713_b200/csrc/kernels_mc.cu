@@ -372,6 +372,13 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
     // (more CTAs per SM still spill: 5 CTAs at 96 registers ran 42% slower)
     constexpr bool SMQ = CONST && CB >= 16;
     __shared__ float4 qsh[SMQ ? NQ : 1];
+    // WQ (time-varying rows at 16 candidates): each warp stages the next
+    // step's row in a shared double buffer (lane l < NQ loads element l), and
+    // every lane reads it from there: one float4 of prefetch per lane instead
+    // of the two 64-register row buffers
+    constexpr bool WQ = !CONST && CB >= 16;
+    __shared__ float4 wq[WQ ? kWarps : 1][2][WQ ? NQ : 1];
+    int wbuf = 0;
     if constexpr (SMQ) {
         if (threadIdx.x < NQ) qsh[threadIdx.x] = crow0[threadIdx.x];
         __syncthreads();
@@ -386,7 +393,9 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
             A[p] = a0[p];
             Y[p] = make_float2(0.0f, 0.0f);
         }
-        if (live) {
+        // WQ: every lane runs the step loop (its __syncwarp needs the whole warp);
+        // a path past num_paths is simulated on an unused stream and never priced
+        if (live || WQ) {
             auto normals = [&](int i, float& z1, float& z2) {
                 uint64_t na, nb;  // the step's two draws, in the reference's order
                 if (P.rng == SABR_RNG_XOSHIRO) {
@@ -404,8 +413,9 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     float2 c1, nc2, rs, ss;
-                    if constexpr (SMQ) {
-                        const float4 qa = lds_f4(qsh + 2 * p), qb = lds_f4(qsh + 2 * p + 1);
+                    if constexpr (SMQ || WQ) {
+                        const float4* src = SMQ ? qsh : wq[WQ ? warp : 0][wbuf];
+                        const float4 qa = lds_f4(src + 2 * p), qb = lds_f4(src + 2 * p + 1);
                         c1 = make_float2(qa.x, qa.y);
                         nc2 = make_float2(qa.z, qa.w);
                         rs = make_float2(qb.x, qb.y);
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
             };
             float4 q[NQ], qn[NQ];
             const float4* crow = crow0;
-            if constexpr (!SMQ) load(qn, crow);
+            if constexpr (!SMQ && !WQ) load(qn, crow);
             float hn = static_cast<float>(-__ldg(hdt) * 1.4426950408889634);
             float z1, z2;
             normals(0, z1, z2);
@@ -452,6 +462,27 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
                     z2 = n2;
                 }
                 advance_all(hn, qn, z1, z2);
+            } else if constexpr (WQ) {
+                if (lane < NQ) wq[warp][0][lane] = __ldg(crow0 + lane);
+                wbuf = 0;
+                __syncwarp();
+                float h = hn;
+                for (int i = 0; i + 1 < n; ++i) {
+                    const float4 pf = lane < NQ ? __ldg(crow0 + static_cast<int64_t>(i + 1) * rstride + lane)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                    hn = static_cast<float>(-__ldg(hdt + i + 1) * 1.4426950408889634);
+                    float n1, n2;
+                    normals(i + 1, n1, n2);
+                    advance_all(h, qn, z1, z2);
+                    if (lane < NQ) wq[warp][wbuf ^ 1][lane] = pf;
+                    __syncwarp();
+                    wbuf ^= 1;
+                    h = hn;
+                    z1 = n1;
+                    z2 = n2;
+                }
+                advance_all(h, qn, z1, z2);
+                __syncwarp();  // the last reads before the next path re-stages buffer 0
             } else {
             // unrolled by 2 so the q <- qn rotation is register renaming;
             // step i+1's row is loaded while step i computes

@@ -102,13 +102,12 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     // candidates per thread: 8 (register bound in FP64; in FP32 the
     // coefficient prefetch buffer takes the room a 16-wide group would need)
     int cb = chunk >= 8 ? 8 : (chunk >= 4 ? 4 : (chunk >= 2 ? 2 : 1));
-    // FP32 with time-invariant rows (C4): 16 candidates per thread, the shared
-    // RNG and Box-Muller amortised over twice the candidates (r02: C4 FP32
-    // 1.24e12 -> 1.52e12 path-steps/s; the time-varying FP32 rows and FP64
-    // spill at 16, 2-3x slower, tools/ab_mc.py with SABR_MC_CB)
-    bool all_const = !job.slices.empty();
-    for (const auto& sl : job.slices) all_const = all_const && sl.const_coef;
-    if (fp32 && all_const && chunk >= 16) cb = 16;
+    // FP32: 16 candidates per thread, the shared RNG and Box-Muller amortised
+    // over twice the candidates, the coefficient rows read from shared memory
+    // (kernels_mc.cu SMQ / WQ) (r02: C4 FP32 1.24e12 -> 1.54e12, C5 FP32
+    // 1.33e12 -> 1.63e12 path-steps/s; FP64 spills at 16, 2x slower,
+    // tools/ab_mc.py with SABR_MC_CB)
+    if (fp32 && chunk >= 16) cb = 16;
     if (const char* e = std::getenv("SABR_MC_CB")) {  // tuning override (1, 2, 4, 8, 16)
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) cb = v;
