@@ -289,9 +289,10 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
 // CTAs per SM of the FP32 kernel: its packed state fits 76 (time-invariant
 // rows) / 95 registers without spills in the step loop at CB <= 8, so 6 / 5
 // CTAs (24 / 20 warps per SM) hide the MUFU and FFMA2 latencies (r02: at 4
-// CTAs ncu showed 1.4 eligible warps per scheduler, "wait" the top stall)
+// CTAs ncu showed 1.4 eligible warps per scheduler, "wait" the top stall);
+// at CB = 16, 4 (time-invariant, SMQ) / 5 (time-varying, WQ + KSM)
 template <int CB, bool CONST>
-constexpr int f32_min_ctas() { return CB <= 8 ? (CONST ? 6 : 5) : 4; }
+constexpr int f32_min_ctas() { return CB <= 8 ? (CONST ? 6 : 5) : (CONST ? 4 : 5); }
 
 // one float4 of shared memory, re-read at every use (asm volatile: the
 // compiler may not keep it in registers across the step loop)
@@ -341,6 +342,22 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
         }
     }
     if (act_mask == 0) return;  // block-uniform
+    // 16 candidates with time-varying rows: the per-pair constants in shared
+    // memory too (KSM), read where used instead of holding 32 registers, so
+    // the kernel fits 96 registers and 5 CTAs per SM (C5 FP32 +7%; in the
+    // time-invariant instantiation the same move cost registers elsewhere)
+    constexpr bool KSM = !CONST && CB >= 16;
+    __shared__ float2 ksh[2][KSM ? NP : 1];  // [0] A at x = 0, [1] beta - 1
+    if constexpr (KSM) {
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                ksh[0][p] = a0[p];
+                ksh[1][p] = bm1[p];
+            }
+        }
+        __syncthreads();
+    }
 
     const bool reduce = P.partials != nullptr;
     double* tb = acc + kWarps * CB * mq * 2 + warp * 32 * kTrStride;
@@ -390,7 +407,7 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
         float2 A[NP], Y[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            A[p] = a0[p];
+            A[p] = KSM ? ksh[0][p] : a0[p];
             Y[p] = make_float2(0.0f, 0.0f);
         }
         // WQ: every lane runs the step loop (its __syncwarp needs the whole warp);
@@ -431,7 +448,17 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
                         rs = make_float2(q[0].z, 0.0f);
                         ss = make_float2(q[0].w, 0.0f);
                     }
-                    const float2 arg = __ffma2_rn(bm1[p], Y[p], A[p]);
+                    float2 b1;
+                    if constexpr (KSM) {
+                        float x, y;
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                                     : "=f"(x), "=f"(y)
+                                     : "r"(static_cast<unsigned>(__cvta_generic_to_shared(&ksh[1][p]))));
+                        b1 = make_float2(x, y);
+                    } else {
+                        b1 = bm1[p];
+                    }
+                    const float2 arg = __ffma2_rn(b1, Y[p], A[p]);
                     float2 nh;  // 2^arg, MUFU.EX2 (flush-to-zero: no denormal rescaling)
                     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh.x) : "f"(arg.x));
                     if constexpr (CB >= 2) asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(nh.y) : "f"(arg.y));
