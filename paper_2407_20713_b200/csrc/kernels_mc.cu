@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
     const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
     const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
 
-    Xoshiro rng;
+    Xoshiro rng{};  // zero state for a path past num_paths (WQ runs its step loop too)
     if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
         rng.init(P.seed, p0 / P.block_size);
         const uint64_t k = (p0 % P.block_size) / P.ppt;
