@@ -164,11 +164,12 @@ cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int3
                            int32_t n_local, int32_t cand_stride, const double* t_end, const double* dt,
                            const double* sdt, int64_t total_steps, void* coef, int fp32 /* 0 FP64, 1 FP32, 2 FP32 pair-interleaved */,
                            cudaStream_t s);
-// the step's feasible candidates compacted (t2_compact_kernel), and their
-// costs / non-finite flags scattered back to their chains
+// the step's feasible candidates compacted (t2_compact_kernel; bad_c, the
+// compacted non-finite flags, zeroed), and their costs / non-finite flags
+// scattered back to their chains
 cudaError_t launch_t2_compact(const uint8_t* active, const double* alpha0, const double* beta, int32_t n,
                               int32_t* idx, double* alpha0_c, double* beta_c, uint8_t* active_c,
-                              int32_t* n_live, cudaStream_t s);
+                              int32_t* n_live, int* bad_c, cudaStream_t s);
 cudaError_t launch_t2_scatter(const int32_t* idx, const int32_t* n_live, int32_t n, const double* cost_c,
                               const int* bad_c, double* cost, int* bad, cudaStream_t s);
 // Metropolis (annealer.cpp:123-134) with the MC costs of this step

@@ -16,6 +16,7 @@
 
 #include "device_common.cuh"
 #include "kernels_mc.hpp"
+#include "pdl.cuh"
 
 namespace sabr_gpu {
 
@@ -120,6 +121,21 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
     for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
     for (int i = threadIdx.x; i < kSinCosTableSize; i += kMcThreads) sctab[i] = P.sctab[i];
     const double2* tab_lane = tab + (lane & (kExpRep - 1));
+    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
+    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+
+    Xoshiro rng;
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        // block b of the plan, mc.cpp:126-127; jump to this thread's first path
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t k = (p0 % P.block_size) / P.ppt;
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
+    // the tables and the streams' jump-ahead do not depend on this step's
+    // candidates: they overlap the preceding kernel under PDL (pdl.cuh)
+    pdl_wait();
 
     // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
     // log space, F = F0 exp(x), alpha = exp(la):
@@ -147,18 +163,6 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
         __syncthreads();
     }
 
-    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
-    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
-
-    Xoshiro rng;
-    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
-        // block b of the plan, mc.cpp:126-127; jump to this thread's first path
-        rng.init(P.seed, p0 / P.block_size);
-        const uint64_t k = (p0 % P.block_size) / P.ppt;
-        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
-        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
-        rng.jump(pl);
-    }
 
     const int64_t cstride = P.cand_stride;
     const StepCoef* __restrict__ crow0 = P.coef + static_cast<int64_t>(sl.step_off) * cstride + c0;
@@ -323,6 +327,20 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
     const int c0 = g * CB;
     const int mq = sl.q_end - sl.q_begin;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
+    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+
+    Xoshiro rng{};  // zero state for a path past num_paths (WQ runs its step loop too)
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t k = (p0 % P.block_size) / P.ppt;
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
+    // the streams' jump-ahead does not depend on this step's candidates: it
+    // overlaps the preceding kernel under PDL (pdl.cuh)
+    pdl_wait();
 
     uint32_t act_mask = 0;
     float2 a0[NP], bm1[NP];
@@ -366,17 +384,6 @@ __global__ void __launch_bounds__(kMcThreads, f32_min_ctas<CB, CONST>())
         __syncthreads();
     }
 
-    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
-    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
-
-    Xoshiro rng{};  // zero state for a path past num_paths (WQ runs its step loop too)
-    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
-        rng.init(P.seed, p0 / P.block_size);
-        const uint64_t k = (p0 % P.block_size) / P.ppt;
-        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
-        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
-        rng.jump(pl);
-    }
 
     // coefficient rows as float4: CB >= 2 two per pair (pair layout), CB = 1 one
     constexpr int NQ = CB >= 2 ? 2 * NP : 1;
@@ -677,6 +684,8 @@ __host__ __device__ inline int reduce_groups(int n_tiles) {
 __global__ void __launch_bounds__(kReduceThreads) mc_reduce_kernel(const McParams P, double* __restrict__ value,
                                                                    double* __restrict__ std_error) {
     __shared__ double2 part[kReduceThreads];
+    pdl_wait();
+    pdl_trigger();
     const int G = blockDim.y, X = blockDim.x;
     const int64_t ncol = static_cast<int64_t>(P.n_cand) * P.n_quotes;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * X + threadIdx.x;
@@ -727,6 +736,8 @@ __global__ void __launch_bounds__(kReduceThreads) mc_reduce_kernel(const McParam
 // case2_mc_cost, calibration.cpp:410-413: sum over slices and quotes in order.
 __global__ void mc_cost_kernel(const McParams P, const double* __restrict__ value,
                                const double* __restrict__ market, double* __restrict__ cost) {
+    pdl_wait();
+    pdl_trigger();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P.n_cand) return;
     if (P.active != nullptr && P.active[c] == 0) return;
@@ -761,8 +772,7 @@ cudaError_t tiles_t(const McParams& p, cudaStream_t s) {
     q.n_groups = n_groups;
     const int64_t blocks = static_cast<int64_t>(q.tile_count) * q.n_slices * n_groups;
     if (blocks <= 0) return cudaSuccess;
-    k<<<static_cast<unsigned>(blocks), kMcThreads, smem, s>>>(q);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3(static_cast<unsigned>(blocks)), dim3(kMcThreads), smem, s, q);
 }
 
 }  // namespace
@@ -857,13 +867,12 @@ cudaError_t launch_mc_reduce(const McParams& p, double* value, double* std_error
     const int64_t n = static_cast<int64_t>(p.n_cand) * p.n_quotes;
     if (n > 0) {
         const int G = reduce_groups(p.n_tiles), X = kReduceThreads / G;
-        mc_reduce_kernel<<<static_cast<unsigned>((n + X - 1) / X), dim3(X, G), 0, s>>>(p, value, std_error);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(mc_reduce_kernel, dim3(static_cast<unsigned>((n + X - 1) / X)), dim3(X, G), 0, s,
+                                   p, value, std_error);
         if (e != cudaSuccess) return e;
     }
     if (cost != nullptr && p.n_cand > 0) {
-        mc_cost_kernel<<<(p.n_cand + 127) / 128, 128, 0, s>>>(p, value, market, cost);
-        return cudaGetLastError();
+        return launch_pdl(mc_cost_kernel, dim3((p.n_cand + 127) / 128), dim3(128), 0, s, p, value, market, cost);
     }
     return cudaSuccess;
 }

@@ -20,6 +20,7 @@
 
 #include "device_common.cuh"
 #include "kernels.hpp"
+#include "pdl.cuh"
 #include "slice_qr.hpp"
 
 namespace sabr_gpu {
@@ -906,10 +907,7 @@ __device__ void reduce_block_records(RedShared<NT>& rs, const SaLevelArgs& a, in
     }
 }
 
-// griddepcontrol (sm_90+): let the dependent grid launch / wait for the
-// prerequisite grid's completion and memory.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// griddepcontrol (sm_90+): pdl_trigger / pdl_wait, pdl.cuh
 
 // --------------------------------------------------------- level kernel ---
 // propose, annealer.cpp:60-74, for one coordinate: bit-identical to the
@@ -1552,6 +1550,8 @@ constexpr int kProposeChainsPerCta = 4;
 __global__ void __launch_bounds__(32 * kProposeChainsPerCta)
     t2_propose_kernel(T2Chain* __restrict__ chains, const sabr_sa_state* st, const T2StepArgs a,
                       double* __restrict__ alpha0, double* __restrict__ beta, uint8_t* __restrict__ active) {
+    pdl_wait();
+    pdl_trigger();
     const int c = blockIdx.x * kProposeChainsPerCta + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (c >= a.n_local) return;  // warp-uniform
@@ -1622,6 +1622,8 @@ __global__ void t2_coef_kernel(const T2Chain* __restrict__ chains, const int32_t
                                const double* __restrict__ sdt, const int64_t total_steps,
                                double4* __restrict__ coef, float4* __restrict__ coef32,
                                const int pairs) {
+    pdl_wait();
+    pdl_trigger();
     if (c0 >= *n_live) return;  // uniform
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<int64_t>(cand_stride) * total_steps) return;
@@ -1659,7 +1661,9 @@ __global__ void __launch_bounds__(kCompactThreads)
     t2_compact_kernel(const uint8_t* __restrict__ active, const double* __restrict__ alpha0,
                       const double* __restrict__ beta, const int32_t n, int32_t* __restrict__ idx,
                       double* __restrict__ alpha0_c, double* __restrict__ beta_c, uint8_t* __restrict__ active_c,
-                      int32_t* __restrict__ n_live) {
+                      int32_t* __restrict__ n_live, int* __restrict__ bad_c) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int32_t warp_tot[kCompactThreads / 32];
     const int seg = (n + kCompactThreads - 1) / kCompactThreads;
     const int b = threadIdx.x * seg, e = min(n, b + seg);
@@ -1702,12 +1706,17 @@ __global__ void __launch_bounds__(kCompactThreads)
         active_c[c] = 0;
     }
     if (threadIdx.x == 0) *n_live = total;
+    // the step's non-finite flags reset here rather than by a memset, which
+    // would break the PDL chain of the step's kernels
+    for (int c = threadIdx.x; c < n; c += kCompactThreads) bad_c[c] = 0;
 }
 
 // The compacted candidates' costs and non-finite flags back to their chains.
 __global__ void t2_scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_live,
                                   const double* __restrict__ cost_c, const int* __restrict__ bad_c,
                                   double* __restrict__ cost, int* __restrict__ bad) {
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *n_live) return;
     const int c = idx[k];
@@ -1739,6 +1748,8 @@ __device__ __forceinline__ void t2_accept_one(T2Chain& ch, double fy, const T2St
 __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs a,
                                  const double* __restrict__ cost, const int* __restrict__ bad,
                                  int* __restrict__ nonfinite) {
+    pdl_wait();
+    pdl_trigger();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.n_local) return;
     T2Chain& ch = chains[c];
@@ -1755,6 +1766,8 @@ __global__ void t2_finish_kernel(T2Chain* __restrict__ chains, const T2StepArgs 
                                  const int32_t* __restrict__ n_live, const double* __restrict__ values,
                                  const int32_t nq, const double* __restrict__ market,
                                  const int* __restrict__ bad_c, int* __restrict__ nonfinite) {
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= *n_live) return;
     T2Chain& ch = chains[idx[k]];
@@ -2103,9 +2116,8 @@ cudaError_t launch_t2_level_init(T2Chain* chains, const sabr_sa_state* st, const
 cudaError_t launch_t2_propose(T2Chain* chains, const sabr_sa_state* st, const T2StepArgs& a,
                               double* alpha0, double* beta, uint8_t* active, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
-    t2_propose_kernel<<<(a.n_local + kProposeChainsPerCta - 1) / kProposeChainsPerCta, 32 * kProposeChainsPerCta, 0,
-                        s>>>(chains, st, a, alpha0, beta, active);
-    return cudaGetLastError();
+    return launch_pdl(t2_propose_kernel, dim3((a.n_local + kProposeChainsPerCta - 1) / kProposeChainsPerCta),
+                      dim3(32 * kProposeChainsPerCta), 0, s, chains, st, a, alpha0, beta, active);
 }
 
 cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int32_t* n_live, int32_t c0,
@@ -2114,42 +2126,40 @@ cudaError_t launch_t2_coef(const T2Chain* chains, const int32_t* idx, const int3
                            cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(cand_stride) * total_steps;
     if (n <= 0) return cudaSuccess;
-    t2_coef_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-        chains, idx, n_live, c0, n_local, cand_stride, t_end, dt, sdt, total_steps,
-        fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr, fp32 == 2);
-    return cudaGetLastError();
+    return launch_pdl(t2_coef_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, chains, idx,
+                      n_live, c0, n_local, cand_stride, t_end, dt, sdt, total_steps,
+                      fp32 ? nullptr : static_cast<double4*>(coef), fp32 ? static_cast<float4*>(coef) : nullptr,
+                      static_cast<int>(fp32 == 2));
 }
 
 cudaError_t launch_t2_compact(const uint8_t* active, const double* alpha0, const double* beta, int32_t n,
                               int32_t* idx, double* alpha0_c, double* beta_c, uint8_t* active_c,
-                              int32_t* n_live, cudaStream_t s) {
+                              int32_t* n_live, int* bad_c, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    t2_compact_kernel<<<1, kCompactThreads, 0, s>>>(active, alpha0, beta, n, idx, alpha0_c, beta_c, active_c,
-                                                    n_live);
-    return cudaGetLastError();
+    return launch_pdl(t2_compact_kernel, dim3(1), dim3(kCompactThreads), 0, s, active, alpha0, beta, n, idx,
+                      alpha0_c, beta_c, active_c, n_live, bad_c);
 }
 
 cudaError_t launch_t2_scatter(const int32_t* idx, const int32_t* n_live, int32_t n, const double* cost_c,
                               const int* bad_c, double* cost, int* bad, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    t2_scatter_kernel<<<(n + 255) / 256, 256, 0, s>>>(idx, n_live, cost_c, bad_c, cost, bad);
-    return cudaGetLastError();
+    return launch_pdl(t2_scatter_kernel, dim3((n + 255) / 256), dim3(256), 0, s, idx, n_live, cost_c, bad_c, cost,
+                      bad);
 }
 
 cudaError_t launch_t2_accept(T2Chain* chains, const T2StepArgs& a, const double* cost,
                              const int* bad, int* nonfinite, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
-    t2_accept_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, a, cost, bad, nonfinite);
-    return cudaGetLastError();
+    return launch_pdl(t2_accept_kernel, dim3((a.n_local + 127) / 128), dim3(128), 0, s, chains, a, cost, bad,
+                      nonfinite);
 }
 
 cudaError_t launch_t2_finish(T2Chain* chains, const T2StepArgs& a, const int32_t* idx, const int32_t* n_live,
                              const double* values, int32_t nq, const double* market, const int* bad_c,
                              int* nonfinite, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
-    t2_finish_kernel<<<(a.n_local + 127) / 128, 128, 0, s>>>(chains, a, idx, n_live, values, nq, market, bad_c,
-                                                             nonfinite);
-    return cudaGetLastError();
+    return launch_pdl(t2_finish_kernel, dim3((a.n_local + 127) / 128), dim3(128), 0, s, chains, a, idx, n_live,
+                      values, nq, market, bad_c, nonfinite);
 }
 
 cudaError_t launch_t2_level_end(const T2Chain* chains, const SaLevelArgs& a, int64_t level,

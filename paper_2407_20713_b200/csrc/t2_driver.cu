@@ -212,6 +212,7 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
     ta.chain_begin = begin;
 
     const bool one_chunk = n_local <= chunk;
+    const int coef_layout = fp32 ? (cb >= 2 ? 2 : 1) : 0;
     Timer timer(ctx);
     timer.start();
     int64_t mc_launches = 0, launches = 0;
@@ -222,17 +223,19 @@ AnnealOut run_sa_case2(sabr_ctx* ctx, const HostSurface& surface, const std::vec
         check_cuda(launch_t2_level_init(chains, a.state, ta, ctx->stream), "t2_level_init");
         for (int step = 0; step < sch.chain_length; ++step) {
             NvtxRange nvtx_step("sabr.t2_step");
+            // the step's kernels form one PDL chain (pdl.cuh): each may be
+            // scheduled while its predecessor runs, and waits for it in-kernel
             check_cuda(launch_t2_propose(chains, a.state, ta, alpha0, beta, active, ctx->stream), "t2_propose");
             // the MC launches run over the compacted feasible candidates: a
             // chunk past the live count exits in every kernel
             check_cuda(launch_t2_compact(active, alpha0, beta, n_local, cidx, alpha0_c, beta_c, active_c, n_live,
-                                         ctx->stream), "t2_compact");
-            check_cuda(cudaMemsetAsync(bad_c, 0, sizeof(int) * nl, ctx->stream), "memset");
+                                         bad_c, ctx->stream), "t2_compact");
+            launches += 2;
             for (int32_t c0 = 0; c0 < n_local; c0 += chunk) {
                 const int32_t nc = std::min(chunk, n_local - c0);
                 const int32_t nc_pad = (nc + cb - 1) / cb * cb;
-                check_cuda(launch_t2_coef(chains, cidx, n_live, c0, nc, nc_pad, d_tend, d_dt, d_sdt, S,
-                                          coef, fp32 ? (cb >= 2 ? 2 : 1) : 0, ctx->stream), "t2_coef");
+                check_cuda(launch_t2_coef(chains, cidx, n_live, c0, nc, nc_pad, d_tend, d_dt, d_sdt, S, coef,
+                                          coef_layout, ctx->stream), "t2_coef");
                 McParams Q = P;
                 Q.n_cand = nc;
                 Q.alpha0 = alpha0_c + c0;

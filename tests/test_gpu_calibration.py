@@ -188,6 +188,28 @@ def test_case2_T2_candidate_block_invariance(engine, eq_surface, precision, case
         assert b.temperature_trace == a.temperature_trace, cb
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_case2_T2_pdl_chain_matches_serialised_launches(engine, eq_surface, precision, monkeypatch):
+    """The kernels of a T_II step (propose, compact, coefficients, MC tiles,
+    reduction, finish) are chained by programmatic dependent launch (pdl.cuh):
+    a kernel may start its stream-independent set-up while its predecessor
+    runs and waits for it in-kernel.  SABR_T2_PDL=0 launches them fully
+    serialised; the report must be bit-identical."""
+    surf = pkg.VolSurface(eq_surface.spot, [eq_surface.slices[2]])
+    fixed = {"a": 0.0, "b": 0.0, "q_rho": 0.0, "q_nu": 0.0, "d_rho": 0.0, "d_nu": 0.0, "beta": 1.0}
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.5, chain_length=3, workers=40, t_min=0.4, seed=6)
+    plan = pkg.SimulationPlan(num_paths=2000, seed=3, precision=precision)
+    reps = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("SABR_T2_PDL", v)
+        reps[v] = engine.calibrate_case2_T2(surf, None, s, plan, fixed)
+    a, b = reps["0"], reps["1"]
+    assert b.evals == a.evals
+    assert b.final_cost == a.final_cost
+    assert b.params == a.params
+    assert b.temperature_trace == a.temperature_trace
+
+
 def test_case2_T2_wide_slice_matches_reference(engine, ref):
     """A slice of 400 quotes: the tile kernel's payoff accumulators outgrow
     shared memory at 8 or 16 candidates per thread, so the engine drops to the
