@@ -121,20 +121,10 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
     for (int i = threadIdx.x; i < kLogTableSize; i += kMcThreads) ltab[i] = P.logtab[i];
     for (int i = threadIdx.x; i < kSinCosTableSize; i += kMcThreads) sctab[i] = P.sctab[i];
     const double2* tab_lane = tab + (lane & (kExpRep - 1));
-    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
-    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
-
-    Xoshiro rng;
-    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
-        // block b of the plan, mc.cpp:126-127; jump to this thread's first path
-        rng.init(P.seed, p0 / P.block_size);
-        const uint64_t k = (p0 % P.block_size) / P.ppt;
-        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
-        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
-        rng.jump(pl);
-    }
-    // the tables and the streams' jump-ahead do not depend on this step's
-    // candidates: they overlap the preceding kernel under PDL (pdl.cuh)
+    // the table staging does not depend on this step's candidates: it
+    // overlaps the preceding kernel under PDL (pdl.cuh).  (The jump-ahead
+    // ahead of the wait too, as in the FP32 kernel, cost the time-varying
+    // 8-candidate instantiation 16 B more stack and C5 FP64 2.5%.)
     pdl_wait();
 
     // Per candidate: ln(alpha) and (beta - 1).  Every candidate is carried in
@@ -163,6 +153,18 @@ __global__ void __launch_bounds__(kMcThreads, 4) mc_tile_kernel(const __grid_con
         __syncthreads();
     }
 
+    const uint64_t tile_paths = static_cast<uint64_t>(kMcThreads) * P.ppt;
+    const uint64_t p0 = static_cast<uint64_t>(tile) * tile_paths + static_cast<uint64_t>(threadIdx.x) * P.ppt;
+
+    Xoshiro rng;
+    if (P.rng == SABR_RNG_XOSHIRO && p0 < P.num_paths) {
+        // block b of the plan, mc.cpp:126-127; jump to this thread's first path
+        rng.init(P.seed, p0 / P.block_size);
+        const uint64_t k = (p0 % P.block_size) / P.ppt;
+        const uint64_t* poly = P.jump + 4 * (sl.jump_off + static_cast<int64_t>(k));
+        uint64_t pl[4] = {poly[0], poly[1], poly[2], poly[3]};
+        rng.jump(pl);
+    }
 
     const int64_t cstride = P.cand_stride;
     const StepCoef* __restrict__ crow0 = P.coef + static_cast<int64_t>(sl.step_off) * cstride + c0;

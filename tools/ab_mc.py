@@ -1,5 +1,6 @@
 """A/B of two engine builds on the MC calibration items (C4 and C5 FP64/FP32,
-kernel path-steps/s), interleaved so clock drift affects both alike:
+path-steps/s of the MC kernels and of the whole run), interleaved so clock
+drift affects both alike:
 
     python tools/ab_mc.py paper_2407_20713_b200/lib/libsabr_b200.so other.so"""
 import os
@@ -24,16 +25,18 @@ def run(eng, what, precision):
     eng.calibrate_case2_T2(surf, bounds, sch, plan, fixed)
     eng.calibrate_case2_T2(surf, bounds, sch, plan, fixed)
     t = eng.last_timing()
-    return t.path_steps / (t.kernel_ms / 1e3)
+    return t.path_steps / (t.kernel_ms / 1e3), t.path_steps / (t.total_ms / 1e3)
 
 
 libs = sys.argv[1:]
 engs = [pkg.Engine(0, lib=_abi.load_library(p)) for p in libs]
+for e in engs:
+    e.set_profiling(True)
 for what in ("c4", "c5"):
     for precision in ("fp64", "fp32"):
         vals = [[] for _ in engs]
         for _ in range(3):
             for i, e in enumerate(engs):
                 vals[i].append(run(e, what, precision))
-        print(what, precision, " | ".join(f"{os.path.basename(libs[i])}: {max(v):.4e}" for i, v in enumerate(vals)),
-              flush=True)
+        print(what, precision, " | ".join(f"{os.path.basename(libs[i])}: kernel {max(k for k, _ in v):.4e} "
+                                          f"run {max(w for _, w in v):.4e}" for i, v in enumerate(vals)), flush=True)
