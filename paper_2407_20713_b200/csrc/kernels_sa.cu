@@ -1760,19 +1760,35 @@ __global__ void t2_accept_kernel(T2Chain* __restrict__ chains, const T2StepArgs 
 
 // A step whose candidates are one MC launch (r02): the candidate's cost
 // (mc_cost_kernel's sum), its chain (t2_scatter) and the Metropolis test
-// (t2_accept) in one kernel, one thread per compacted candidate - the same
-// arithmetic, two launches fewer per SA step.
-__global__ void t2_finish_kernel(T2Chain* __restrict__ chains, const T2StepArgs a, const int32_t* __restrict__ idx,
-                                 const int32_t* __restrict__ n_live, const double* __restrict__ values,
-                                 const int32_t nq, const double* __restrict__ market,
-                                 const int* __restrict__ bad_c, int* __restrict__ nonfinite) {
+// (t2_accept) in one kernel, two launches fewer per SA step.  One warp per
+// compacted candidate: the lanes load the quotes and form the relative errors
+// side by side, then every lane adds their squares in quote order from warp
+// broadcasts, sum = fma(rel, rel, sum) - mc_quote_cost's contracted sum, bit
+// for bit - and lane 0 runs the Metropolis test.
+constexpr int kFinishWarps = 4;
+__global__ void __launch_bounds__(32 * kFinishWarps)
+    t2_finish_kernel(T2Chain* __restrict__ chains, const T2StepArgs a, const int32_t* __restrict__ idx,
+                     const int32_t* __restrict__ n_live, const double* __restrict__ values, const int32_t nq,
+                     const double* __restrict__ market, const int* __restrict__ bad_c, int* __restrict__ nonfinite) {
     pdl_wait();
     pdl_trigger();
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= *n_live) return;
+    const int k = blockIdx.x * kFinishWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (k >= *n_live) return;  // warp-uniform
+    const double* v = values + static_cast<int64_t>(k) * nq;
+    double sum = 0.0;
+    for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int q = q0 + lane;
+        const double rel = q < nq ? (market[q] - v[q]) / market[q] : 0.0;
+        const int n = min(32, nq - q0);
+        for (int j = 0; j < n; ++j) {
+            const double r = __shfl_sync(0xffffffffu, rel, j);
+            sum = fma(r, r, sum);
+        }
+    }
+    if (lane != 0) return;
     T2Chain& ch = chains[idx[k]];
     if (bad_c[k]) atomicOr(nonfinite, 1);
-    t2_accept_one(ch, mc_quote_cost(values + static_cast<int64_t>(k) * nq, market, nq), a);
+    t2_accept_one(ch, sum, a);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -2158,8 +2174,8 @@ cudaError_t launch_t2_finish(T2Chain* chains, const T2StepArgs& a, const int32_t
                              const double* values, int32_t nq, const double* market, const int* bad_c,
                              int* nonfinite, cudaStream_t s) {
     if (a.n_local <= 0) return cudaSuccess;
-    return launch_pdl(t2_finish_kernel, dim3((a.n_local + 127) / 128), dim3(128), 0, s, chains, a, idx, n_live,
-                      values, nq, market, bad_c, nonfinite);
+    return launch_pdl(t2_finish_kernel, dim3((a.n_local + kFinishWarps - 1) / kFinishWarps), dim3(32 * kFinishWarps),
+                      0, s, chains, a, idx, n_live, values, nq, market, bad_c, nonfinite);
 }
 
 cudaError_t launch_t2_level_end(const T2Chain* chains, const SaLevelArgs& a, int64_t level,
