@@ -234,6 +234,22 @@ SABR_API sabr_status sabr_calibrate_static_T1(sabr_ctx* ctx, const sabr_surface*
                                               const sabr_schedule* schedule,
                                               const sabr_fixed* fixed, sabr_report* report);
 
+/* calibrate_static_T1 on n slices of one surface at once: reports[i] is
+ * exactly what sabr_calibrate_static_T1(ctx, surface, slices[i], ...) returns.
+ * Replaces a caller's loop over slices (e.g. proj/tools/sabr_cli.cpp:70 run
+ * per slice).  On a single-rank context every slice's annealer runs on its own
+ * stream (a child context of ctx, created on first use) from its own host
+ * thread, so the level kernels of independent slices share the SMs (a C2
+ * slice's level grid alone holds 7 of the 10 one-warp CTAs an SM can run);
+ * the child streams are ordered after ctx's stream and ctx's stream after
+ * them.  Multi-rank contexts run the slices one after another.  The first
+ * failing slice's status is returned (its message in sabr_last_error). */
+SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_surface* surface,
+                                                     const int64_t* slices, int64_t n,
+                                                     const sabr_bounds* bounds,
+                                                     const sabr_schedule* schedule,
+                                                     const sabr_fixed* fixed, sabr_report* reports);
+
 /* calibrate_dynamic_case1_T1, calibration.hpp:88-91 / calibration.cpp:325-365 */
 SABR_API sabr_status sabr_calibrate_dynamic_case1_T1(sabr_ctx* ctx,
                                                      const sabr_surface* surface,

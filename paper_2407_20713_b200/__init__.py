@@ -10,6 +10,6 @@ from .api import (AnnealingSchedule, AnnealResult, CalibrationReport, CaseIIPara
                   PriceEstimate, ReportRow, SabrError, SimulationPlan, StaticSabrParams,
                   VolQuote, VolSlice, VolSurface, black_scholes_call, calibrate_case2_formula,
                   calibrate_case2_T2, calibrate_dynamic_case1_T1, calibrate_static_T1,
-                  default_engine, evaluate_case1, evaluate_case2_prices, n_levels, parse_surface)
+                  calibrate_static_T1_slices, default_engine, evaluate_case1, evaluate_case2_prices, n_levels, parse_surface)
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -183,7 +183,8 @@ LIB_PATH = os.path.join(PKG_DIR, "lib", "libsabr_b200.so")
 EXPORTS = [
     "sabr_last_error", "sabr_version", "sabr_ctx_create", "sabr_ctx_destroy",
     "sabr_ctx_set_profiling", "sabr_ctx_last_timing", "sabr_comm_unique_id",
-    "sabr_ctx_init_comm", "sabr_calibrate_static_T1", "sabr_calibrate_dynamic_case1_T1",
+    "sabr_ctx_init_comm", "sabr_calibrate_static_T1", "sabr_calibrate_static_T1_slices",
+    "sabr_calibrate_dynamic_case1_T1",
     "sabr_calibrate_case2_T2", "sabr_calibrate_case2_formula", "sabr_evaluate_case1",
     "sabr_evaluate_case2_prices", "sabr_cost_batch", "sabr_implied_vol_batch",
     "sabr_case2_feasible_batch", "sabr_mc_simulate_terminals",

@@ -482,6 +482,30 @@ class Engine:
                                                       C.byref(rb.rep)))
         return rb.report()
 
+    def calibrate_static_T1_slices(self, surface: VolSurface, slices=None, bounds=None,
+                                   schedule: Optional[AnnealingSchedule] = None, fixed=None,
+                                   trace: bool = False) -> List[CalibrationReport]:
+        """calibrate_static_T1 for each of `slices` (default: every slice) in
+        one call; on a single-rank engine the slices' annealers run side by side
+        on their own streams (sabr_calibrate_static_T1_slices).  Reports equal
+        the one-slice calls'."""
+        schedule = schedule or AnnealingSchedule()
+        idx = list(range(len(surface.slices))) if slices is None else [int(i) for i in slices]
+        s, keep = surface.to_abi()
+        b, kb = _bounds_abi(bounds)
+        f, kf = _fixed_abi(fixed)
+        bufs = [_ReportBuf(surface.total_quotes(), n_levels(schedule) if trace else 0) for _ in idx]
+        reps = (A.sabr_report * max(1, len(idx)))()
+        for i, rb in enumerate(bufs):
+            reps[i] = rb.rep
+        sl = (C.c_int64 * max(1, len(idx)))(*idx)
+        sch = schedule.to_abi()
+        self._check(self.lib.sabr_calibrate_static_T1_slices(self._ctx, C.byref(s), sl, C.c_int64(len(idx)),
+                                                             C.byref(b), C.byref(sch), C.byref(f), reps))
+        for i, rb in enumerate(bufs):
+            rb.rep = reps[i]
+        return [rb.report() for rb in bufs]
+
     def calibrate_dynamic_case1_T1(self, surface: VolSurface, bounds=None,
                                    schedule: Optional[AnnealingSchedule] = None, fixed=None,
                                    trace: bool = False) -> CalibrationReport:
@@ -723,6 +747,10 @@ def black_scholes_call(spot, strike, rate, dividend, maturity, vol) -> float:
 
 def calibrate_static_T1(surface, slice, bounds=None, schedule=None, fixed=None):
     return default_engine().calibrate_static_T1(surface, slice, bounds, schedule, fixed)
+
+
+def calibrate_static_T1_slices(surface, slices=None, bounds=None, schedule=None, fixed=None):
+    return default_engine().calibrate_static_T1_slices(surface, slices, bounds, schedule, fixed)
 
 
 def calibrate_dynamic_case1_T1(surface, bounds=None, schedule=None, fixed=None):

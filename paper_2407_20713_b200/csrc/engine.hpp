@@ -45,6 +45,8 @@ struct sabr_ctx {
     // per-launch event pairs of the dominant kernel when profiling
     std::vector<cudaEvent_t> kev;
     size_t kev_used = 0;
+    // child contexts (own streams) of sabr_calibrate_static_T1_slices
+    std::vector<sabr_ctx*> children;
 };
 
 namespace sabr_gpu {

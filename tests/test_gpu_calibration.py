@@ -39,6 +39,29 @@ def test_static_T1_matches_reference(engine, ref, eq_surface, seed):
     assert g.seed == seed
 
 
+def test_static_T1_slices_match_one_slice_calls(engine, fx_surface):
+    """sabr_calibrate_static_T1_slices runs each slice's annealer on its own
+    stream and host thread; every report must equal the one-slice call's, bit
+    for bit (parameters, cost, evals, rows, temperature trace), for all slices,
+    a reordered subset, and repeated calls (the child contexts are reused)."""
+    s = pkg.AnnealingSchedule(t0=2.0, cooling=0.8, chain_length=20, workers=500, groups=4, t_min=1e-3, seed=3)
+    single = [engine.calibrate_static_T1(fx_surface, i, None, s, None, trace=True)
+              for i in range(len(fx_surface.slices))]
+    for sel in (None, [2, 0], [3]):
+        for _ in range(2):
+            multi = engine.calibrate_static_T1_slices(fx_surface, sel, None, s, None, trace=True)
+            idx = list(range(len(fx_surface.slices))) if sel is None else sel
+            assert len(multi) == len(idx)
+            for i, m in zip(idx, multi):
+                g = single[i]
+                assert m.evals == g.evals and m.final_cost == g.final_cost and m.params == g.params
+                assert m.temperature_trace == g.temperature_trace
+                assert [(r.strike, r.model) for r in m.rows] == [(r.strike, r.model) for r in g.rows]
+    with pytest.raises(pkg.OutOfRangeError):
+        engine.calibrate_static_T1_slices(fx_surface, [0, 9], None, s, None)
+    assert engine.calibrate_static_T1_slices(fx_surface, [], None, s, None) == []
+
+
 def test_static_T1_fixed_and_bounds(engine, ref, fx_surface):
     s = pkg.AnnealingSchedule(t0=1.0, cooling=0.8, chain_length=10, workers=4, t_min=1e-2, seed=1)
     g = engine.calibrate_static_T1(fx_surface, 0, {"nu": (0.01, 3.0)}, s, {"beta": 0.75, "rho": -0.4})
