@@ -345,7 +345,8 @@ def run_ours(args):
                    "l2": "flushed (256 MB write) before every timed step",
                    "parallelism": f"chains sharded over {world} GPU(s), one 240-byte record all-gather per level; "
                                   + ("the 4 slices' calibrations side by side on 4 streams "
-                                     "(calibrate_static_T1_slices)" if world == 1 else "slices one after another"),
+                                     "(calibrate_static_T1_slices)" if world == 1 or transport.startswith("fused")
+                                     else "slices one after another (per-level transport all-gather)"),
                    "transport": transport},
         "e2e": {"value": e2e, "unit": "cost-evals/s",
                 "h2d_bytes_per_step": len(fx.slices) * (surface_bytes(pkg.VolSurface(fx.spot, [fx.slices[0]])) + 4 * 8 + 400),

@@ -242,8 +242,11 @@ SABR_API sabr_status sabr_calibrate_static_T1(sabr_ctx* ctx, const sabr_surface*
  * thread, so the level kernels of independent slices share the SMs (a C2
  * slice's level grid alone holds 7 of the 10 one-warp CTAs an SM can run);
  * the child streams are ordered after ctx's stream and ctx's stream after
- * them.  Multi-rank contexts run the slices one after another.  The first
- * failing slice's status is returned (its message in sabr_last_error). */
+ * them.  Multi-rank contexts with the peer exchange enabled do the same (each
+ * child gets its own peer mailboxes, set up over ctx's transport; collective:
+ * every rank makes the same call); with the per-level transport all-gather the
+ * slices run one after another.  The first failing slice's status is
+ * returned (its message in sabr_last_error). */
 SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_surface* surface,
                                                      const int64_t* slices, int64_t n,
                                                      const sabr_bounds* bounds,

@@ -220,6 +220,22 @@ using RunAllFn = std::function<cudaError_t(const SaLevelArgs&, const double*, in
 // `start` seeds incumbent/best values on the device, `level` launches one
 // temperature level (whose last CTA merges, or which writes the rank record
 // for the NCCL merge).  `records` = CTA records one level kernel writes.
+// All ranks' exchange modes must agree (one all-gather, also a barrier).
+void mode_consensus(sabr_ctx* ctx, uint64_t mine) {
+    auto* dsend = static_cast<uint64_t*>(dev_buf(ctx, "mode_send", sizeof(uint64_t)));
+    auto* drecv = static_cast<uint64_t*>(dev_buf(ctx, "mode_recv", sizeof(uint64_t) * ctx->nranks));
+    check_cuda(cudaMemcpyAsync(dsend, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream), "H2D mode");
+    allgather(ctx, dsend, drecv, sizeof(uint64_t));
+    std::vector<uint64_t> modes(ctx->nranks);
+    check_cuda(cudaMemcpyAsync(modes.data(), drecv, sizeof(uint64_t) * ctx->nranks, cudaMemcpyDeviceToHost,
+                               ctx->stream), "D2H modes");
+    sync(ctx);
+    for (int r = 0; r < ctx->nranks; ++r)
+        if (modes[r] != mine)
+            fail(SABR_E_INVALID, "exchange mode differs between ranks (enable/disable the peer exchange on "
+                                 "every rank)");
+}
+
 T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std::vector<double>& lo,
                      const std::vector<double>& hi, const std::vector<double>& start_full,
                      const sabr_schedule& sch, bool start_ok, int64_t records,
@@ -296,26 +312,14 @@ T1Out run_sa_generic(sabr_ctx* ctx, int dim_full, uint32_t free_mask, const std:
 
     // fused peer exchange (all ranks decide alike: every rank has chains iff n_chains >= nranks)
     const bool peer = ctx->peer && ctx->nranks > 1 && n_chains >= ctx->nranks && use_peer;
-    if (ctx->nranks > 1) {
-        // Every rank must run the same exchange mode: a rank on the peer
-        // mailboxes and a rank in the per-level all-gather would wait on each
-        // other.  One all-gather of the mode byte over the transport, which
-        // doubles as a barrier before level 0, so the mailbox timeout below
-        // starts with every rank inside the run.
-        const uint64_t mine = peer ? 1u : 0u;
-        auto* dsend = static_cast<uint64_t*>(dev_buf(ctx, "mode_send", sizeof(uint64_t)));
-        auto* drecv = static_cast<uint64_t*>(dev_buf(ctx, "mode_recv", sizeof(uint64_t) * ctx->nranks));
-        check_cuda(cudaMemcpyAsync(dsend, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream), "H2D mode");
-        allgather(ctx, dsend, drecv, sizeof(uint64_t));
-        std::vector<uint64_t> modes(ctx->nranks);
-        check_cuda(cudaMemcpyAsync(modes.data(), drecv, sizeof(uint64_t) * ctx->nranks, cudaMemcpyDeviceToHost,
-                                   ctx->stream), "D2H modes");
-        sync(ctx);
-        for (int r = 0; r < ctx->nranks; ++r)
-            if (modes[r] != mine)
-                fail(SABR_E_INVALID, "exchange mode differs between ranks (enable/disable the peer exchange on "
-                                     "every rank)");
-    }
+    // Every rank must run the same exchange mode: a rank on the peer
+    // mailboxes and a rank in the per-level all-gather would wait on each
+    // other.  One all-gather of the mode byte over the transport, which
+    // doubles as a barrier before level 0, so the mailbox timeout below
+    // starts with every rank inside the run.  (A child context of
+    // sabr_calibrate_static_T1_slices borrows its parent's transport; the
+    // parent ran this check for all of them before the children started.)
+    if (ctx->nranks > 1 && !ctx->child) mode_consensus(ctx, peer ? 1u : 0u);
     if (peer) {
         a.peer_boxes = ctx->peer_boxes;
         a.my_rank = ctx->rank;
@@ -1105,7 +1109,10 @@ SABR_API sabr_status sabr_ctx_create(int32_t device, void* stream, sabr_ctx** ou
 
 SABR_API void sabr_ctx_destroy(sabr_ctx* ctx) {
     if (!ctx) return;
-    for (sabr_ctx* c : ctx->children) sabr_ctx_destroy(c);
+    for (sabr_ctx* c : ctx->children) {
+        c->comm = nullptr;  // borrowed from ctx
+        sabr_ctx_destroy(c);
+    }
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->bufs)
@@ -1342,7 +1349,13 @@ SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_s
         msg.assign(static_cast<size_t>(n), std::string());
         if (n == 0) return;
         const auto t0 = std::chrono::steady_clock::now();
-        if (ctx->nranks > 1 || n == 1) {  // the transport serves one run at a time
+        // side by side: one rank, or ranks exchanging through peer mailboxes
+        // (each child its own, so no run touches the shared transport); the
+        // per-level transport all-gather serves one run at a time
+        const bool side_by_side =
+            n > 1 && (ctx->nranks == 1 || (ctx->peer && schedule != nullptr &&
+                                           static_cast<int64_t>(schedule->workers) * schedule->groups >= ctx->nranks));
+        if (!side_by_side) {
             sabr_timing sum{};
             for (int64_t i = 0; i < n; ++i) {
                 st[i] = sabr_calibrate_static_T1_locked(ctx, surface, slices[i], bounds, schedule, fixed,
@@ -1363,7 +1376,23 @@ SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_s
         while (ctx->children.size() < static_cast<size_t>(n)) {
             sabr_ctx* c = nullptr;
             if (sabr_ctx_create(ctx->device, nullptr, &c) != SABR_OK) fail(SABR_E_CUDA, g_last_error);
+            c->child = true;
             ctx->children.push_back(c);
+        }
+        if (ctx->nranks > 1) {
+            // the children borrow the transport for their mailbox set-up only
+            // (collective: every rank enables child 0, 1, ... in this order),
+            // then one mode check on the parent is the barrier before level 0
+            for (int64_t i = 0; i < n; ++i) {
+                sabr_ctx* c = ctx->children[i];
+                c->rank = ctx->rank;
+                c->nranks = ctx->nranks;
+                c->comm = ctx->comm;
+                c->exchange = ctx->exchange;
+                c->exchange_user = ctx->exchange_user;
+                if (!c->peer && sabr_ctx_enable_peer_exchange(c) != SABR_OK) fail(SABR_E_NCCL, g_last_error);
+            }
+            mode_consensus(ctx, 2u);
         }
         // the children start after ctx's stream's prior work
         check_cuda(cudaEventRecord(ctx->ev0, ctx->stream), "event record");

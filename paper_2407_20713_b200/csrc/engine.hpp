@@ -45,8 +45,11 @@ struct sabr_ctx {
     // per-launch event pairs of the dominant kernel when profiling
     std::vector<cudaEvent_t> kev;
     size_t kev_used = 0;
-    // child contexts (own streams) of sabr_calibrate_static_T1_slices
+    // child contexts (own streams) of sabr_calibrate_static_T1_slices; a
+    // child of a multi-rank context borrows its transport and has its own
+    // peer mailboxes
     std::vector<sabr_ctx*> children;
+    bool child = false;
 };
 
 namespace sabr_gpu {

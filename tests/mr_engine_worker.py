@@ -34,6 +34,10 @@ def workloads(eng):
     out = {}
     s = pkg.AnnealingSchedule(t0=2.0, cooling=0.85, chain_length=40, workers=301, groups=3, t_min=1e-4, seed=7)
     out["static"] = report_key(eng.calibrate_static_T1(fx, 1, None, s, None, trace=True))
+    # every slice in one call: side by side on child streams (one rank, or
+    # ranks on peer mailboxes: each child its own), else one after another
+    for i, r in enumerate(eng.calibrate_static_T1_slices(fx, [3, 1, 0], None, s, None, trace=True)):
+        out[f"static_slices_{i}"] = report_key(r)
     cap = pkg.AnnealingSchedule(t0=2.0, cooling=0.8, chain_length=50, workers=77, groups=2, t_min=1e-2, seed=9,
                                 max_evals=20000)
     out["static_cap"] = report_key(eng.calibrate_static_T1(eq, 0, None, cap, {"beta": 0.9}, trace=True))
