@@ -237,10 +237,11 @@ SABR_API sabr_status sabr_calibrate_static_T1(sabr_ctx* ctx, const sabr_surface*
 /* calibrate_static_T1 on n slices of one surface at once: reports[i] is
  * exactly what sabr_calibrate_static_T1(ctx, surface, slices[i], ...) returns.
  * Replaces a caller's loop over slices (e.g. proj/tools/sabr_cli.cpp:70 run
- * per slice).  On a single-rank context every slice's annealer runs on its own
- * stream (a child context of ctx, created on first use) from its own host
- * thread, so the level kernels of independent slices share the SMs (a C2
- * slice's level grid alone holds 7 of the 10 one-warp CTAs an SM can run);
+ * per slice).  On a single-rank context the slices' annealers run side by
+ * side on up to 8 streams (child contexts of ctx, created on first use, one
+ * host thread each, each running its share of the slices in order), so the
+ * level kernels of independent slices share the SMs (a C2 slice's level grid
+ * alone holds 7 of the 10 one-warp CTAs an SM can run);
  * the child streams are ordered after ctx's stream and ctx's stream after
  * them.  Multi-rank contexts with the peer exchange enabled do the same (each
  * child gets its own peer mailboxes, set up over ctx's transport; collective:

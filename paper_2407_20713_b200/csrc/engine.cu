@@ -1373,7 +1373,11 @@ SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_s
             ctx->timing = sum;
             return;
         }
-        while (ctx->children.size() < static_cast<size_t>(n)) {
+        // at most kMaxSideBySide streams: worker w runs slices w, w + W, ...
+        // in order (the same order on every rank)
+        constexpr int64_t kMaxSideBySide = 8;
+        const int64_t W = std::min(n, kMaxSideBySide);
+        while (ctx->children.size() < static_cast<size_t>(W)) {
             sabr_ctx* c = nullptr;
             if (sabr_ctx_create(ctx->device, nullptr, &c) != SABR_OK) fail(SABR_E_CUDA, g_last_error);
             c->child = true;
@@ -1383,8 +1387,8 @@ SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_s
             // the children borrow the transport for their mailbox set-up only
             // (collective: every rank enables child 0, 1, ... in this order),
             // then one mode check on the parent is the barrier before level 0
-            for (int64_t i = 0; i < n; ++i) {
-                sabr_ctx* c = ctx->children[i];
+            for (int64_t w = 0; w < W; ++w) {
+                sabr_ctx* c = ctx->children[w];
                 c->rank = ctx->rank;
                 c->nranks = ctx->nranks;
                 c->comm = ctx->comm;
@@ -1396,29 +1400,38 @@ SABR_API sabr_status sabr_calibrate_static_T1_slices(sabr_ctx* ctx, const sabr_s
         }
         // the children start after ctx's stream's prior work
         check_cuda(cudaEventRecord(ctx->ev0, ctx->stream), "event record");
-        for (int64_t i = 0; i < n; ++i) {
-            ctx->children[i]->profiling = ctx->profiling;
-            check_cuda(cudaStreamWaitEvent(ctx->children[i]->stream, ctx->ev0, 0), "stream wait");
+        for (int64_t w = 0; w < W; ++w) {
+            ctx->children[w]->profiling = ctx->profiling;
+            check_cuda(cudaStreamWaitEvent(ctx->children[w]->stream, ctx->ev0, 0), "stream wait");
         }
+        std::vector<sabr_timing> tm(static_cast<size_t>(n));
         std::vector<std::thread> th;
-        th.reserve(static_cast<size_t>(n));
-        for (int64_t i = 0; i < n; ++i)
-            th.emplace_back([&, i] {
-                st[i] = sabr_calibrate_static_T1(ctx->children[i], surface, slices[i], bounds, schedule, fixed,
-                                                 reports + i);
-                if (st[i] != SABR_OK) msg[i] = g_last_error;
+        th.reserve(static_cast<size_t>(W));
+        for (int64_t w = 0; w < W; ++w)
+            th.emplace_back([&, w] {
+                sabr_ctx* c = ctx->children[w];
+                for (int64_t i = w; i < n; i += W) {
+                    st[i] = sabr_calibrate_static_T1(c, surface, slices[i], bounds, schedule, fixed, reports + i);
+                    tm[i] = c->timing;
+                    if (st[i] != SABR_OK) {
+                        msg[i] = g_last_error;
+                        break;
+                    }
+                }
             });
         for (auto& t : th) t.join();
         // ctx's stream continues after the children's work
         sabr_timing sum{};
-        for (int64_t i = 0; i < n; ++i) {
-            sabr_ctx* c = ctx->children[i];
+        for (int64_t w = 0; w < W; ++w) {
+            sabr_ctx* c = ctx->children[w];
             check_cuda(cudaEventRecord(c->ev1, c->stream), "event record");
             check_cuda(cudaStreamWaitEvent(ctx->stream, c->ev1, 0), "stream wait");
-            sum.units += c->timing.units;
-            sum.kernel_ms += c->timing.kernel_ms;
-            sum.kernel_launches += c->timing.kernel_launches;
-            sum.total_launches += c->timing.total_launches;
+        }
+        for (const sabr_timing& t : tm) {
+            sum.units += t.units;
+            sum.kernel_ms += t.kernel_ms;
+            sum.kernel_launches += t.kernel_launches;
+            sum.total_launches += t.total_launches;
         }
         sum.total_ms = 1e3 * seconds_since(t0);
         ctx->timing = sum;

@@ -57,6 +57,12 @@ def test_static_T1_slices_match_one_slice_calls(engine, fx_surface):
                 assert m.evals == g.evals and m.final_cost == g.final_cost and m.params == g.params
                 assert m.temperature_trace == g.temperature_trace
                 assert [(r.strike, r.model) for r in m.rows] == [(r.strike, r.model) for r in g.rows]
+    # more slices than side-by-side streams (8): each stream runs its share in order
+    many = list(range(len(fx_surface.slices))) * 3
+    for i, m in enumerate(engine.calibrate_static_T1_slices(fx_surface, many, None, s, None, trace=True)):
+        g = single[i % len(fx_surface.slices)]
+        assert m.evals == g.evals and m.final_cost == g.final_cost and m.params == g.params
+        assert m.temperature_trace == g.temperature_trace
     with pytest.raises(pkg.OutOfRangeError):
         engine.calibrate_static_T1_slices(fx_surface, [0, 9], None, s, None)
     assert engine.calibrate_static_T1_slices(fx_surface, [], None, s, None) == []
